@@ -1,0 +1,451 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 hot path of arXiv 2004.04049 (OSPR + GS with LUT phase
+randomisation), BASELINE.json metric "OSPR 1024^2 binary sub-frames/s & GS
+iters/s; achieved HBM GB/s vs peak".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl holo|reference]
+
+One step = one pass of every hot-path row of SURVEY.md §8(a) over one batch:
+  OSPR (headline `value`): BASELINE configs[2] (C3) -- a0 LUT build (L = 2^16 by
+  default) + a1-a7 for one frame set of N_SF = 24 binary 1024x1024 sub-frames
+  (holograms, mean replay intensity, MSE), inputs resident in HBM.
+  GS (`gs` block): BASELINE configs[3] (C4) -- 64 frames x 50 iterations at
+  1024x1024, continuous phase-only, LUT 2^16.
+Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier and
+torch.cuda.synchronize(); L2 is flushed (256 MiB write) before every timed step;
+CUDA events on the launching stream; max over ranks.  Multi-GPU (torchrun): OSPR
+sub-frames are sharded across ranks and the partial intensity sums are combined
+with an NCCL all-reduce before the MSE (strong scaling); GS frames are sharded
+(no collective).  `--impl reference` times the fp64 CPU oracle (oracle/) on the
+host cores on the same workload (the paper has no GPU implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "OSPR 1024^2 binary sub-frames/s"
+UNIT = "sub-frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["holo", "reference"], default="holo")
+    ap.add_argument("--lut", type=int, default=1 << 16, help="headline LUT length")
+    ap.add_argument("--no-gs", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gs-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                mhz.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------------
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def shard(n_units, world, rank):
+    b = (n_units * rank) // world
+    e = (n_units * (rank + 1)) // world
+    return b, e
+
+
+def timed_loop(step_fn, k, w, world, flush):
+    """W warm-up steps, then K timed steps, each: flush L2, barrier + sync, events."""
+    import torch
+    for _ in range(w):
+        step_fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    total = 0.0
+    per = []
+    for _ in range(k):
+        flush()
+        barrier(world)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        step_fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = a.elapsed_time(b)
+        per.append(ms)
+        total += ms
+    return total, per
+
+
+def run_gpu(args):
+    import torch
+    import paper_2004_04049_b200 as hb
+    from holo_synth import LUT_SEED, WORKLOADS, target_for
+
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    props = torch.cuda.get_device_properties(dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+
+    # ---------------- OSPR C3 ----------------
+    w3 = WORKLOADS["C3"]
+    n, S, P = w3.n, w3.n_sub, w3.n * w3.n
+    T = torch.from_numpy(target_for(w3)).to(dev)
+    sb, se = shard(S, world, rank)
+    full = (world == 1)
+    ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device=dev)
+    lut_buf = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
+    out = hb.OsprResult(bits=torch.empty((1, se - sb, n, n // 8), dtype=torch.uint8, device=dev),
+                        intensity=torch.empty((1, n, n), dtype=torch.float32, device=dev),
+                        mse=torch.empty(1, dtype=torch.float64, device=dev) if full else None)
+    mean_buf = torch.empty((1, n, n), dtype=torch.float32, device=dev)
+    mse_buf = torch.empty(1, dtype=torch.float64, device=dev)
+
+    def make_ospr_step(L, lut):
+        def step():
+            hb.lut_generate(LUT_SEED, L, out=lut[:L])                       # a0
+            hb.ospr_generate(T, S, lut[:L], sf_range=(sb, se), workspace=ws, out=out)   # a1-a7
+            if not full:
+                import torch.distributed as dist
+                dist.all_reduce(out.intensity)                              # C-1: sum of partial I
+                hb.ospr_finalize(T, out.intensity, S, out=mean_buf)         # a7 after the reduce
+        return step
+
+    step = make_ospr_step(args.lut, lut_buf)
+    l0 = hb.launch_count()
+    with Clocks(local) as clk:
+        total_ms, per = timed_loop(step, args.steps, args.warmup, world, flush)
+    launches = (hb.launch_count() - l0)
+    launches_timed = launches * args.steps // (args.steps + args.warmup)
+    total_ms = max_over_ranks(total_ms, world)
+    ms_step = total_ms / args.steps
+    value = S * args.steps / (total_ms / 1e3)
+
+    # per-kernel device time over a second pass of K steps with event bracketing
+    hb.profile_enable(True)
+    for _ in range(args.steps):
+        flush()
+        step()
+    torch.cuda.synchronize()
+    kern = {}
+    for name in hb.kernel_names():
+        cnt, ms = hb.profile_read(name)
+        if cnt:
+            kern[name] = {"launches": cnt, "total_ms": ms, "avg_us": 1e3 * ms / cnt}
+    hb.profile_enable(False)
+    step_kernel_ms = sum(v["total_ms"] for v in kern.values()) / args.steps
+
+    # roofline of the dominant kernel (algorithmic bytes per launch)
+    chunk = max(1, min(16, (64 << 20) // (P * 8), (S + 1) // 2))
+    npairs = (se - sb + 1) // 2
+    nchunks = -(-npairs // chunk)
+    pairs_per_launch = npairs / nchunks
+    bytes_per_pair = {
+        "ospr_rows_a": 4 * P + 8 * P + 2 * 8 * min(args.lut, P),   # T, Z out, LUT entries touched
+        "ospr_cols": 8 * P + 8 * P + P // 4,                        # Z in/out, 2 bit planes
+        "ospr_rows_c": 8 * P,                                       # X in (+ acc RMW per chunk)
+    }
+    dom = max((k for k in kern if k in bytes_per_pair), key=lambda k: kern[k]["total_ms"])
+    per_launch = bytes_per_pair[dom] * pairs_per_launch + (8 * P / 1 if dom == "ospr_rows_c" else 0)
+    achieved = per_launch / (kern[dom]["avg_us"] * 1e-6) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    share = kern[dom]["total_ms"] / args.steps / step_kernel_ms
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian-blob targets, holo_synth; stands in for USC-SIPI images)",
+        "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step (a0 LUT build + "
+                               "a1-a7 incl. MSE); BASELINE configs[2]",
+                   "n": n, "n_sub": S, "lut_len": args.lut, "lut_seed": LUT_SEED,
+                   "l2": "flushed before every timed step (256 MiB write)",
+                   "parallelism": f"sub-frame shards x{world}" + (" + NCCL all-reduce of intensity" if world > 1 else "")},
+        "gpu_launches": launches_timed,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": kern[dom]["avg_us"],
+                     "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "kernels": kern,
+        "clocks": clk.summary(),
+        "device": {"name": props.name, "sms": props.multi_processor_count,
+                   "l2_mb": getattr(props, "L2_cache_size", 0) / 2 ** 20},
+    }
+
+    # ---------------- LUT sweep of C3 ----------------
+    if not args.no_sweep and world == 1:
+        sweep = {}
+        big = torch.empty(max(w3.lut_lens), dtype=torch.complex64, device=dev)
+        for L in w3.lut_lens:
+            st = make_ospr_step(L, big)
+            tm, _ = timed_loop(st, max(3, args.steps // 2), 2, world, flush)
+            sweep[str(L)] = {"sub_frames_per_s": S * max(3, args.steps // 2) / (tm / 1e3),
+                             "ms_per_step": tm / max(3, args.steps // 2), "mse": float(out.mse.item())}
+        result["lut_sweep"] = sweep
+        del big
+
+    # ---------------- e2e through the public API with host buffers ----------------
+    if not args.no_e2e:
+        T_host = torch.from_numpy(target_for(w3)).pin_memory()
+        bits_host = torch.empty(out.bits.shape, dtype=torch.uint8).pin_memory()
+        mse_host = torch.empty(1, dtype=torch.float64).pin_memory()
+        T_dev = torch.empty_like(T)
+        lut_e2e = hb.lut_generate(LUT_SEED, args.lut, device=dev)
+
+        def e2e_step():
+            T_dev.copy_(T_host, non_blocking=True)                              # H2D inputs
+            hb.ospr_generate(T_dev, S, lut_e2e, sf_range=(sb, se), workspace=ws, out=out)
+            if not full:
+                import torch.distributed as dist
+                dist.all_reduce(out.intensity)
+                _, m = hb.ospr_finalize(T_dev, out.intensity, S, out=mean_buf)
+                mse_host.copy_(m, non_blocking=True)
+            else:
+                mse_host.copy_(out.mse, non_blocking=True)                      # D2H metric
+            bits_host.copy_(out.bits, non_blocking=True)                        # D2H holograms
+        tm, _ = timed_loop(e2e_step, args.steps, args.warmup, world, flush)
+        tm = max_over_ranks(tm, world)
+        result["e2e"] = {"value": S * args.steps / (tm / 1e3), "unit": UNIT,
+                         "h2d_bytes_per_step": T_host.numel() * 4,
+                         "d2h_bytes_per_step": bits_host.numel() + 8,
+                         "what": "pinned host target -> device, ospr_generate, packed holograms + MSE -> host"}
+
+    # ---------------- GS C4 ----------------
+    if not args.no_gs:
+        w4 = WORKLOADS["C4"]
+        B, iters, n4 = w4.frames, w4.iters, w4.n
+        fb, fe = shard(B, world, rank)
+        T4 = torch.from_numpy(np.stack([target_for(w4, b) for b in range(fb, fe)])).to(dev)
+        lut4 = torch.empty(1 << 16, dtype=torch.complex64, device=dev)
+        ws4 = torch.empty(hb.gs_workspace_bytes(n4, fe - fb, iters), dtype=torch.uint8, device=dev)
+        gout = hb.GsResult(holo=torch.empty((fe - fb, n4, n4), dtype=torch.complex64, device=dev), levels=None,
+                           intensity=torch.empty((fe - fb, n4, n4), dtype=torch.float32, device=dev),
+                           mse=torch.empty((fe - fb, iters), dtype=torch.float64, device=dev),
+                           err_e=torch.empty((fe - fb, iters), dtype=torch.float64, device=dev))
+
+        def gs_step():
+            hb.lut_generate(LUT_SEED, 1 << 16, out=lut4)
+            hb.gs_generate(T4, iters, lut4, phase_offset=fb * n4 * n4, levels=0, workspace=ws4, out=gout)
+
+        ks = args.gs_steps or max(3, args.steps // 4)
+        hb.profile_enable(True)
+        gm, _ = timed_loop(gs_step, ks, min(args.warmup, 3), world, flush)
+        gk = {}
+        for name in ("gs_rows_init", "gs_cols", "gs_rows", "mse_reduce", "lut_generate"):
+            cnt, ms = hb.profile_read(name)
+            if cnt:
+                gk[name] = {"launches": cnt, "total_ms": ms, "avg_us": 1e3 * ms / cnt}
+        hb.profile_enable(False)
+        gm = max_over_ranks(gm, world)
+        P4 = n4 * n4
+        g = min(16, max(1, (32 << 20) // (P4 * 8)), fe - fb)
+        gbytes = {"gs_cols": 16 * P4 * g, "gs_rows": 20 * P4 * g}
+        gdom = max(gbytes, key=lambda k: gk.get(k, {"total_ms": 0})["total_ms"])
+        gach = gbytes[gdom] / (gk[gdom]["avg_us"] * 1e-6) / 1e9
+        result["gs"] = {
+            "metric": "GS 1024^2 iterations/s", "unit": "frame-iterations/s",
+            "value": B * iters * ks / (gm / 1e3), "ms_per_step": gm / ks, "steps": ks,
+            "config": {"workload": "C4: GS 1024x1024, 64 frames x 50 iterations, continuous phase-only, "
+                                   "LUT 2^16; BASELINE configs[3]", "frames_per_rank": fe - fb},
+            "roofline": {"bound": "hbm", "kernel": gdom, "achieved": gach, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": gach / hbm_peak, "algorithmic_bytes_per_launch": gbytes[gdom],
+                         "avg_launch_us": gk[gdom]["avg_us"]},
+            "kernels": gk,
+        }
+
+    if rank == 0 and world == 1:
+        result["cpu_baseline"] = cpu_baseline(args.lut)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------------------------
+def _oracle_frame_set(T, lut, S, region, threads):
+    """The oracle as it stands on one C3 frame set: one thread per sub-frame
+    (or_ospr_subframe releases the GIL through ctypes), then mean + M-1 MSE."""
+    import oracle
+    n = T.shape[0]
+
+    def one(s):
+        return oracle.ospr_subframe(T, lut, s * n * n, want_h=False, want_intensity=True)[2]
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        Is = list(ex.map(one, range(S)))
+    I = np.sum(Is, axis=0) / S
+    return oracle.mse_m1(I, T, region)
+
+
+def cpu_baseline(L, steps=1):
+    import oracle
+    from holo_synth import LUT_SEED, WORKLOADS, target_for
+    w3 = WORKLOADS["C3"]
+    T = target_for(w3)
+    lut = oracle.lut_build(LUT_SEED, L)
+    threads = min(w3.n_sub, os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _oracle_frame_set(T, lut, w3.n_sub, w3.omega().as_tuple(), threads)
+    dt = time.perf_counter() - t0
+    return {"value": w3.n_sub * steps / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{steps} full C3 frame set(s): {w3.n_sub} sub-frames of 1024^2 (apply_phase, radix-2 "
+                      f"fp64 IDFT, sign, DFT, |.|^2) + mean + MSE, L={L}, one thread per sub-frame; "
+                      f"host nproc={os.cpu_count()}",
+            "seconds": dt}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from holo_synth import LUT_SEED, WORKLOADS, target_for
+    oracle.build()
+    w3 = WORKLOADS["C3"]
+    T = target_for(w3)
+    lut = oracle.lut_build(LUT_SEED, args.lut)
+    threads = min(w3.n_sub, os.cpu_count() or 1)
+    steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    for _ in range(warm):
+        _oracle_frame_set(T, lut, w3.n_sub, w3.omega().as_tuple(), threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _oracle_frame_set(T, lut, w3.n_sub, w3.omega().as_tuple(), threads)
+    dt = time.perf_counter() - t0
+    v = w3.n_sub * steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step; BASELINE configs[2]",
+                   "lut_len": args.lut},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{steps} C3 frame set(s) of 24 sub-frames (steps capped at 3 to bound CPU "
+                                   f"time), one thread per sub-frame, host nproc={os.cpu_count()}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

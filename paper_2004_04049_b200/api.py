@@ -1,0 +1,240 @@
+"""Python binding of libholo with the C ABI's names (include/holo.h).
+
+Argument marshalling only: tensors are passed by ``data_ptr()`` together with
+the current CUDA stream; every step of the hot path runs in the library's
+sm_100a kernels.  torch supplies device memory and streams, nothing else.
+
+Conventions (see include/holo.h): targets are float32 CUDA tensors
+[frames][N][N]; complex fields and the LUT are complex64 (interleaved fp32
+re, im); OSPR holograms are packed bits uint8 [frames][sub-frames][N][N/8].
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from ._lib import HoloRegion, check, lib
+
+__all__ = [
+    "lut_generate", "ospr_workspace_bytes", "ospr_generate", "ospr_finalize", "gs_workspace_bytes",
+    "gs_generate", "gs_step", "fft2", "debug_randomise", "launch_count", "profile_enable", "profile_read",
+    "kernel_names", "version", "default_omega", "OsprResult", "GsResult",
+]
+
+
+def version() -> str:
+    return lib().holo_version().decode()
+
+
+def _stream(dev: torch.device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def default_omega(n: int, algo: str) -> Tuple[int, int, int, int]:
+    """R-13: OSPR measures rows [1, N/2) x all columns; GS the full plane."""
+    return (1, n // 2, 0, n) if algo == "ospr" else (0, n, 0, n)
+
+
+def _region(om: Sequence[int]) -> HoloRegion:
+    return HoloRegion(*[int(v) for v in om])
+
+
+def _lut_args(lut: Optional[torch.Tensor]):
+    if lut is None or lut.numel() == 0:
+        return None, 0
+    _need(lut, torch.complex64, "lut")
+    return lut.data_ptr(), lut.numel()
+
+
+# ---- a0 --------------------------------------------------------------------------------------
+
+def lut_generate(seed: int, n_lut: int, device=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The phase pool: complex64 [n_lut] = (cos, sin) of 2 pi u_k / 2^32 (R-3..R-5)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if out is None:
+        out = torch.empty(n_lut, dtype=torch.complex64, device=dev)
+    _need(out, torch.complex64, "out")
+    check(lib().holo_lut_generate(seed & 0xFFFFFFFFFFFFFFFF, n_lut, out.data_ptr(), _stream(out.device)))
+    return out
+
+
+# ---- OSPR --------------------------------------------------------------------------------------
+
+@dataclass
+class OsprResult:
+    bits: Optional[torch.Tensor]        # uint8 [F][S][N][N/8] (S = shard size)
+    intensity: torch.Tensor             # float32 [F][N][N] (mean, or partial sum for a shard)
+    mse: Optional[torch.Tensor]         # float64 [F]
+
+
+def ospr_workspace_bytes(n: int, n_frames: int, n_sub: int) -> int:
+    return int(lib().holo_ospr_workspace_size(n, n_frames, n_sub))
+
+
+def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] = None, phase_offset: int = 0,
+                  sf_range: Optional[Tuple[int, int]] = None, want_bits: bool = True, want_mse: bool = True,
+                  omega: Optional[Sequence[int]] = None, workspace: Optional[torch.Tensor] = None,
+                  out: Optional[OsprResult] = None) -> OsprResult:
+    """OSPR over target [F][N][N] (or [N][N]); see holo_ospr_generate."""
+    _need(target, torch.float32, "target")
+    t3 = target if target.dim() == 3 else target.unsqueeze(0)
+    F, n, _ = t3.shape
+    b, e = sf_range if sf_range is not None else (0, n_sub)
+    full = (b == 0 and e == n_sub)
+    om = omega if omega is not None else default_omega(n, "ospr")
+    dev = t3.device
+    if out is None:
+        out = OsprResult(
+            bits=torch.empty((F, e - b, n, n // 8), dtype=torch.uint8, device=dev) if want_bits else None,
+            intensity=torch.empty((F, n, n), dtype=torch.float32, device=dev),
+            mse=torch.empty(F, dtype=torch.float64, device=dev) if (want_mse and full) else None)
+    need = ospr_workspace_bytes(n, F, n_sub)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    lp, L = _lut_args(lut)
+    check(lib().holo_ospr_generate(t3.data_ptr(), n, F, n_sub, lp, L, phase_offset, b, e, _ptr(out.bits),
+                                   out.intensity.data_ptr(), _ptr(out.mse), _region(om), workspace.data_ptr(),
+                                   workspace.numel(), _stream(dev)))
+    return out
+
+
+def ospr_finalize(target: torch.Tensor, intensity_sum: torch.Tensor, n_sub: int,
+                  omega: Optional[Sequence[int]] = None, want_mse: bool = True,
+                  out: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
+    """Mean intensity (= sum / n_sub; in place if out is intensity_sum) and MSE."""
+    _need(target, torch.float32, "target")
+    _need(intensity_sum, torch.float32, "intensity_sum")
+    t3 = target if target.dim() == 3 else target.unsqueeze(0)
+    F, n, _ = t3.shape
+    om = omega if omega is not None else default_omega(n, "ospr")
+    out = torch.empty_like(intensity_sum) if out is None else out
+    mse = torch.empty(F, dtype=torch.float64, device=t3.device) if want_mse else None
+    ws = torch.empty(592 * 5 * 8, dtype=torch.uint8, device=t3.device)
+    check(lib().holo_ospr_finalize(t3.data_ptr(), intensity_sum.data_ptr(), n, F, n_sub, _region(om),
+                                   out.data_ptr(), _ptr(mse), ws.data_ptr(), ws.numel(), _stream(t3.device)))
+    return out, mse
+
+
+# ---- GS ------------------------------------------------------------------------------------------
+
+@dataclass
+class GsResult:
+    holo: Optional[torch.Tensor]        # complex64 [B][N][N]
+    levels: Optional[torch.Tensor]      # uint8 [B][N][N]
+    intensity: Optional[torch.Tensor]   # float32 [B][N][N]
+    mse: Optional[torch.Tensor]         # float64 [B][iters]
+    err_e: Optional[torch.Tensor]       # float64 [B][iters]
+
+
+def gs_workspace_bytes(n: int, batch: int, iters: int) -> int:
+    return int(lib().holo_gs_workspace_size(n, batch, iters))
+
+
+def gs_generate(target: torch.Tensor, iters: int, lut: Optional[torch.Tensor] = None, phase_offset: int = 0,
+                levels: int = 0, want_holo: bool = True, want_levels: bool = False, want_intensity: bool = True,
+                want_mse: bool = True, want_err: bool = True, omega: Optional[Sequence[int]] = None,
+                workspace: Optional[torch.Tensor] = None, out: Optional[GsResult] = None) -> GsResult:
+    """GS over target [B][N][N] (or [N][N]); see holo_gs_generate."""
+    _need(target, torch.float32, "target")
+    t3 = target if target.dim() == 3 else target.unsqueeze(0)
+    B, n, _ = t3.shape
+    om = omega if omega is not None else default_omega(n, "gs")
+    dev = t3.device
+    if out is None:
+        out = GsResult(
+            holo=torch.empty((B, n, n), dtype=torch.complex64, device=dev) if want_holo else None,
+            levels=torch.empty((B, n, n), dtype=torch.uint8, device=dev) if want_levels else None,
+            intensity=torch.empty((B, n, n), dtype=torch.float32, device=dev) if want_intensity else None,
+            mse=torch.empty((B, iters), dtype=torch.float64, device=dev) if want_mse else None,
+            err_e=torch.empty((B, iters), dtype=torch.float64, device=dev) if want_err else None)
+    need = gs_workspace_bytes(n, B, iters)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    lp, L = _lut_args(lut)
+    check(lib().holo_gs_generate(t3.data_ptr(), n, B, iters, lp, L, phase_offset, levels, _ptr(out.holo),
+                                 _ptr(out.levels), _ptr(out.intensity), _ptr(out.mse), _ptr(out.err_e),
+                                 _region(om), workspace.data_ptr(), workspace.numel(), _stream(dev)))
+    return out
+
+
+def gs_step(r_in: torch.Tensor, target: torch.Tensor, levels: int = 0, omega: Optional[Sequence[int]] = None):
+    """One GS iteration from R_{k-1} (complex64 [B][N][N]); returns (R_k, GsResult)."""
+    _need(r_in, torch.complex64, "r_in")
+    _need(target, torch.float32, "target")
+    t3 = target if target.dim() == 3 else target.unsqueeze(0)
+    r3 = r_in if r_in.dim() == 3 else r_in.unsqueeze(0)
+    B, n, _ = t3.shape
+    om = omega if omega is not None else default_omega(n, "gs")
+    dev = t3.device
+    r_out = torch.empty_like(r3)
+    res = GsResult(holo=torch.empty_like(r3),
+                   levels=torch.empty((B, n, n), dtype=torch.uint8, device=dev) if 2 <= levels <= 256 else None,
+                   intensity=torch.empty((B, n, n), dtype=torch.float32, device=dev),
+                   mse=torch.empty((B, 1), dtype=torch.float64, device=dev),
+                   err_e=torch.empty((B, 1), dtype=torch.float64, device=dev))
+    need = gs_workspace_bytes(n, B, 1)
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    check(lib().holo_gs_step(r3.data_ptr(), t3.data_ptr(), n, B, levels, r_out.data_ptr(), res.holo.data_ptr(),
+                             _ptr(res.levels), res.intensity.data_ptr(), res.mse.data_ptr(), res.err_e.data_ptr(),
+                             _region(om), ws.data_ptr(), ws.numel(), _stream(dev)))
+    return r_out, res
+
+
+# ---- hooks -------------------------------------------------------------------------------------------
+
+def fft2(x: torch.Tensor, inverse: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Unitary 2D DFT (Eq. (1)) or IDFT (Eq. (2)) of complex64 [B][N][N] / [N][N]."""
+    _need(x, torch.complex64, "x")
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    B, n, _ = x3.shape
+    out = torch.empty_like(x3) if out is None else out
+    check(lib().holo_fft2(x3.data_ptr(), out.data_ptr(), n, B, int(inverse), _stream(x3.device)))
+    return out if x.dim() == 3 else out[0]
+
+
+def debug_randomise(target: torch.Tensor, lut: Optional[torch.Tensor], offset: int) -> torch.Tensor:
+    """Step a2 alone: R = T * lut[(offset + p) mod N_LUT] (flat if lut is None)."""
+    _need(target, torch.float32, "target")
+    n = target.shape[-1]
+    out = torch.empty((n, n), dtype=torch.complex64, device=target.device)
+    lp, L = _lut_args(lut)
+    check(lib().holo_debug_randomise(target.data_ptr(), n, lp, L, offset, out.data_ptr(), _stream(target.device)))
+    return out
+
+
+# ---- instrumentation -------------------------------------------------------------------------------------
+
+def launch_count() -> int:
+    return int(lib().holo_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    check(lib().holo_profile_enable(int(on)))
+
+
+def profile_read(name: str) -> Tuple[int, float]:
+    n = C.c_uint64(0)
+    ms = C.c_double(0.0)
+    check(lib().holo_profile_read(name.encode(), C.byref(n), C.byref(ms)))
+    return int(n.value), float(ms.value)
+
+
+def kernel_names():
+    return lib().holo_kernel_names().decode().split(",")

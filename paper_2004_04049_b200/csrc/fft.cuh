@@ -1,0 +1,230 @@
+// fft.cuh -- the register/shared-memory FFT machinery of libholo (sm_100a).
+//
+// Evaluates the unitary DFT pair of PAPER.md Eqs. (1)-(2) up to the
+// 1/sqrt(N) scale, which the callers fold into their epilogues.
+//
+// A length-N transform (N = R1*R2, R1 <= R2, both powers of two) is done by
+// T = R1 cooperating threads, each holding E = R2 complex values in registers,
+// in two Stockham passes with one exchange through shared memory:
+//   pass 1: thread t holds x[t + R1*m], m < R2, and runs Q = R2/R1 radix-R1
+//           DFTs over the slots {b + Q*r}, writing y[(t + R1*b)*R1 + r];
+//   pass 2: thread t reads y[t + R1*r], r < R2, multiplies by W_N^{r*t} and runs
+//           one radix-R2 DFT; output element t + R1*r lands in slot r.
+// Input and output use the same thread<->element map, so a transform can be
+// followed by another one in registers (OSPR column pass: IFFT -> sign -> FFT).
+// The exchange index i is stored at (i + i/R1)*IL: the +i/R1 pad makes both the
+// strided pass-1 stores and the contiguous pass-2 loads bank-conflict free, and
+// IL interleaves the buffers of IL independent columns (column kernels).
+//
+// The radix-R DFTs are compile-time codelets (recursive radix-4/radix-2 DIT)
+// whose twiddles W_R^k are constexpr; the trivial ones (1, -1, +-i, (+-1+-i)/sqrt2)
+// cost no multiplies.
+#pragma once
+
+#include "common.cuh"
+
+namespace holo {
+namespace fft {
+
+// ---- compile-time trigonometry (for codelet twiddles only) --------------------------------
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+constexpr double sin_red(double x)
+{
+    double s = x * x, t = x, r = x;
+    for (int i = 1; i <= 12; ++i) {
+        t *= -s / ((2.0 * i) * (2.0 * i + 1.0));
+        r += t;
+    }
+    return r;
+}
+constexpr double cos_red(double x)
+{
+    double s = x * x, t = 1.0, r = 1.0;
+    for (int i = 1; i <= 12; ++i) {
+        t *= -s / ((2.0 * i - 1.0) * (2.0 * i));
+        r += t;
+    }
+    return r;
+}
+
+struct CS {
+    double c, s;
+};
+
+// cos, sin of 2*pi*k/n by exact octant reduction of the rational k/n.
+constexpr CS cs2pi(long long k, long long n)
+{
+    k %= n;
+    if (k < 0)
+        k += n;
+    long long e = 8 * k;
+    long long o = e / n;
+    long long rem = e - o * n;
+    double f = (o & 1) ? (double)(n - rem) / (double)n : (double)rem / (double)n;
+    double x = f * (kPi / 4.0);
+    double S = sin_red(x), C = cos_red(x);
+    switch (o) {
+    case 0: return CS{C, S};
+    case 1: return CS{S, C};
+    case 2: return CS{-S, C};
+    case 3: return CS{-C, S};
+    case 4: return CS{-C, -S};
+    case 5: return CS{-S, -C};
+    case 6: return CS{S, -C};
+    default: return CS{C, -S};
+    }
+}
+
+// x * W_R^K with W_R = exp(-2 pi i / R) (forward) or exp(+2 pi i / R) (inverse).
+template <int R, int K, bool INV>
+__device__ __forceinline__ float2 tw_mul(float2 x)
+{
+    constexpr int k = ((K % R) + R) % R;
+    if constexpr (k == 0) {
+        return x;
+    } else if constexpr (2 * k == R) {
+        return make_float2(-x.x, -x.y);
+    } else if constexpr (4 * k == R) {          // fwd -i, inv +i
+        return INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+    } else if constexpr (4 * k == 3 * R) {      // fwd +i, inv -i
+        return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
+    } else if constexpr ((8 * k) % R == 0) {    // odd multiples of pi/4
+        constexpr CS w = cs2pi(INV ? k : -k, R);
+        constexpr float sc = w.c > 0 ? 1.0f : -1.0f;
+        constexpr float ss = w.s > 0 ? 1.0f : -1.0f;
+        constexpr float h = 0.70710678118654752440f;
+        return make_float2((sc * x.x - ss * x.y) * h, (ss * x.x + sc * x.y) * h);
+    } else {
+        constexpr CS w = cs2pi(INV ? k : -k, R);
+        constexpr float c = (float)w.c, s = (float)w.s;
+        return make_float2(x.x * c - x.y * s, x.x * s + x.y * c);
+    }
+}
+
+// In-place DFT of the R values v[0], v[S], ..., v[(R-1)S] (natural order in and out).
+template <int R, int S, bool INV>
+struct Dft {
+    template <int K>
+    static __device__ __forceinline__ void comb4(float2 *v, float2 *t)
+    {
+        if constexpr (K < R / 4) {
+            float2 a = v[4 * S * K];
+            float2 b = tw_mul<R, K, INV>(v[S + 4 * S * K]);
+            float2 c = tw_mul<R, 2 * K, INV>(v[2 * S + 4 * S * K]);
+            float2 d = tw_mul<R, 3 * K, INV>(v[3 * S + 4 * S * K]);
+            float2 apc = cadd(a, c), amc = csub(a, c), bpd = cadd(b, d), bmd = csub(b, d);
+            // W_4 * (b - d): forward W_4 = -i, inverse +i
+            float2 wbmd = INV ? make_float2(-bmd.y, bmd.x) : make_float2(bmd.y, -bmd.x);
+            t[K] = cadd(apc, bpd);
+            t[K + R / 4] = cadd(amc, wbmd);
+            t[K + R / 2] = csub(apc, bpd);
+            t[K + 3 * R / 4] = csub(amc, wbmd);
+            comb4<K + 1>(v, t);
+        }
+    }
+    template <int K>
+    static __device__ __forceinline__ void comb2(float2 *v, float2 *t)
+    {
+        if constexpr (K < R / 2) {
+            float2 a = v[2 * S * K];
+            float2 b = tw_mul<R, K, INV>(v[S + 2 * S * K]);
+            t[K] = cadd(a, b);
+            t[K + R / 2] = csub(a, b);
+            comb2<K + 1>(v, t);
+        }
+    }
+    static __device__ __forceinline__ void run(float2 *v)
+    {
+        if constexpr (R == 1) {
+        } else if constexpr (R == 2) {
+            float2 a = v[0], b = v[S];
+            v[0] = cadd(a, b);
+            v[S] = csub(a, b);
+        } else if constexpr (R % 4 == 0) {
+            Dft<R / 4, 4 * S, INV>::run(v);
+            Dft<R / 4, 4 * S, INV>::run(v + S);
+            Dft<R / 4, 4 * S, INV>::run(v + 2 * S);
+            Dft<R / 4, 4 * S, INV>::run(v + 3 * S);
+            float2 t[R];
+            comb4<0>(v, t);
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                v[S * i] = t[i];
+        } else {
+            Dft<R / 2, 2 * S, INV>::run(v);
+            Dft<R / 2, 2 * S, INV>::run(v + S);
+            float2 t[R];
+            comb2<0>(v, t);
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                v[S * i] = t[i];
+        }
+    }
+};
+
+// ---- plan ---------------------------------------------------------------------------------
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+template <int N>
+struct Plan {
+    static_assert(N >= 16 && N <= 2048 && (N & (N - 1)) == 0, "N must be a power of two in [16, 2048]");
+    static constexpr int LOG = ilog2(N);
+    static constexpr int R1 = 1 << (LOG / 2);       // threads per transform
+    static constexpr int R2 = N / R1;               // values per thread (E)
+    static constexpr int E = R2;
+    static constexpr int T = R1;
+    static constexpr int Q = R2 / R1;               // pass-1 DFTs per thread (1 or 2)
+    static constexpr int SMEM = N + N / R1;         // padded exchange buffer, complex elements
+    static constexpr int TW_OFFSET = N - 16;        // offset of this N in the twiddle pool
+};
+
+// Pass-2 twiddles: g_tw[TW_OFFSET(N) + r*R1 + t] = W_N^{r*t} (forward sign), r < R2, t < R1.
+// Laid out r-major so that the R1 threads of a transform read consecutive entries.
+// Pool size: sum over N = 16..2048 of N = 4080 entries.  Built once per device by
+// holo::fft::twiddles() (host libm in double, rounded to fp32) in library-owned
+// device memory; kernels receive the pool pointer as an argument.
+constexpr int kTwPool = 4096;
+holo_status twiddles(const float2 **pool);
+
+__device__ __forceinline__ int pad_index(int i, int r1) { return i + i / r1; }
+
+// Two-pass FFT of one length-N transform held by T = R1 threads (see header).
+// `sm` points at this transform's exchange buffer (element i at sm[(i + i/R1)*IL]).
+// All threads of the CTA must call this together (it contains __syncthreads()).
+template <int N, bool INV, int IL>
+__device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, int t,
+                                         const float2 *__restrict__ twp)
+{
+    using P = Plan<N>;
+    constexpr int R1 = P::R1, R2 = P::R2, Q = P::Q;
+#pragma unroll
+    for (int b = 0; b < Q; ++b)
+        Dft<R1, Q, INV>::run(v + b);
+    __syncthreads();                        // previous readers of sm are done
+#pragma unroll
+    for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+            const int i = (t + R1 * b) * R1 + r;
+            sm[(i + t + R1 * b) * IL] = v[b + Q * r];   // i/R1 == t + R1*b
+        }
+    __syncthreads();
+    const float2 *tw = twp + P::TW_OFFSET + t;
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+        const int i = t + R1 * r;
+        float2 x = sm[(i + r) * IL];                       // i/R1 == r
+        if (r > 0) {
+            float2 w = __ldg(tw + r * R1);
+            if (INV)
+                w.y = -w.y;
+            x = cmul(x, w);
+        }
+        v[r] = x;
+    }
+    Dft<R2, 1, INV>::run(v);
+}
+
+} // namespace fft
+} // namespace holo

@@ -1,0 +1,487 @@
+// gs.cu -- Gerchberg-Saxton (Fig. 2 left; steps g0-g6 of
+// DESIGN.md §1) as two fused FFT passes per iteration over groups of frames
+// whose state stays L2-resident across iterations.
+//
+//   gs_rows_init  g0: R_0 = T * lut[(base_b + p) mod L] (or a given R_{k-1} for the
+//                 one-step hook); row IFFT -> state; fp64 sums of T^2, T^4 over Omega.
+//   gs_cols       column IFFT -> H_k; g2 constraint (H/|H| or nearest of Q levels);
+//                 last iteration writes h / level outputs; column FFT -> state.
+//   gs_rows       row FFT -> R'_k (x 1/N); g4: I_k = |R'_k|^2, fp64 partial sums of
+//                 I, I^2, I T^2 over Omega and (|R'_k| - T)^2 over the plane;
+//                 g5: R_k = T R'_k/|R'_k|; row IFFT -> state (or R_k / I_k outputs).
+//
+// The 1/sqrt(N) factors of the inverse transforms are dropped: the constraint
+// and the amplitude replacement are invariant to a positive scale.
+#include "fft.cuh"
+
+namespace holo {
+
+constexpr int kMaxGroup = 16;
+
+template <int N>
+struct GsRowCfg {
+    using P = fft::Plan<N>;
+    static constexpr int RPC = (N >= 2048) ? 4 : ((256 / P::T) < N ? (256 / P::T) : N);
+    static constexpr int THREADS = RPC * P::T;
+    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
+    static constexpr int NBLK = N / RPC;   // CTAs per frame
+};
+
+template <int N>
+struct GsColCfg {
+    using P = fft::Plan<N>;
+    static constexpr int W = 8;
+    static constexpr int THREADS = W * P::T;
+    static constexpr size_t SMEM = (size_t)W * P::SMEM * sizeof(float2);
+};
+
+struct FrameBases {
+    uint32_t b[kMaxGroup];
+};
+
+__device__ __forceinline__ void block_reduce_n(double *s, int nvals, double *dst)
+{
+    __shared__ double red[32][4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = 0; i < nvals; ++i) {
+        double x = s[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0)
+            red[w][i] = x;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int i = 0; i < nvals; ++i) {
+            double x = lane < nw ? red[lane][i] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                x += __shfl_down_sync(0xffffffffu, x, o);
+            if (lane == 0)
+                dst[i] = x;
+        }
+    }
+}
+
+__device__ __forceinline__ bool in_region(int y, int x, const holo_region &om)
+{
+    return y >= om.row0 && y < om.row1 && x >= om.col0 && x < om.col1;
+}
+
+// ---- init: R_0 (or R_in) -> row IFFT ---------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(GsRowCfg<N>::THREADS)
+gs_rows_init_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix, FrameBases fb,
+                    const float2 *__restrict__ r_in, int nframes, holo_region om, float2 *__restrict__ state,
+                    double *__restrict__ tparts)
+{
+    using P = fft::Plan<N>;
+    using C = GsRowCfg<N>;
+    constexpr int R1 = P::R1, E = P::E, RPC = C::RPC;
+    extern __shared__ float2 smem[];
+    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
+    const int fr = blockIdx.x / C::NBLK, blk = blockIdx.x % C::NBLK;
+    const int y = blk * RPC + lr;
+    const float *Ty = T + ((size_t)fr * N + y) * N;
+    float2 v[E];
+    double s[2] = {0.0, 0.0};
+    if (r_in != nullptr) {
+        const float2 *Ry = r_in + ((size_t)fr * N + y) * N;
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = Ry[t + R1 * m];
+    } else if (lut != nullptr) {
+        const uint32_t ry = ix.mod_any((uint64_t)fb.b[fr] + (uint64_t)y * N);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int x = t + R1 * m;
+            const float tt = __ldg(Ty + x);
+            const float2 c = lut_at(lut, ix.mod(ry + x));
+            v[m] = make_float2(tt * c.x, tt * c.y);
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = make_float2(__ldg(Ty + t + R1 * m), 0.0f);
+    }
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int x = t + R1 * m;
+        if (in_region(y, x, om)) {
+            const double tt = __ldg(Ty + x), t2 = tt * tt;
+            s[0] += t2;
+            s[1] += t2 * t2;
+        }
+    }
+    fft::fft2pass<N, true, 1>(v, smem + lr * P::SMEM, t, tw);
+    float2 *out = state + ((size_t)fr * N + y) * N;
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        out[t + R1 * r] = v[r];
+    block_reduce_n(s, 2, tparts + ((size_t)fr * C::NBLK + blk) * 2);
+}
+
+// ---- column pass: IFFT -> constraint -> FFT ----------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(GsColCfg<N>::THREADS)
+gs_cols_kernel(const float2 *__restrict__ tw, float2 *__restrict__ state, int levels, float2 *__restrict__ holo, uint8_t *__restrict__ lev)
+{
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E, W = GsColCfg<N>::W;
+    extern __shared__ float2 smem[];
+    const int c = threadIdx.x % W, t = threadIdx.x / W;
+    const int tile = blockIdx.x, fr = blockIdx.y;
+    const size_t fofs = (size_t)fr * N * N;
+    float2 *col = state + fofs + tile * W + c;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+        v[m] = col[(size_t)(t + R1 * m) * N];
+    fft::fft2pass<N, true, W>(v, smem + c, t, tw);            // H_k (x N)
+    const float q_over_2pi = (float)levels * 0.15915494309189533577f;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const float2 h = v[r];
+        float2 o;
+        int j = 0;
+        if (levels == 0) {
+            const float m2 = h.x * h.x + h.y * h.y;
+            if (m2 == 0.0f) {
+                o = make_float2(1.0f, 0.0f);               // R-16: H = 0 -> +1
+            } else {
+                const float rr = rsqrtf(m2);
+                o = make_float2(h.x * rr, h.y * rr);
+            }
+        } else {
+            float th = atan2f(h.y, h.x);
+            if (th < 0.0f)
+                th += 6.28318530717958647692f;
+            j = (int)floorf(th * q_over_2pi + 0.5f);
+            if (j >= levels)
+                j -= levels;
+            double sn, cs;
+            sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
+            o = make_float2((float)cs, (float)sn);
+        }
+        if (holo != nullptr)
+            holo[fofs + (size_t)(t + R1 * r) * N + tile * W + c] = o;
+        if (lev != nullptr)
+            lev[fofs + (size_t)(t + R1 * r) * N + tile * W + c] = (uint8_t)j;
+        v[r] = o;
+    }
+    fft::fft2pass<N, false, W>(v, smem + c, t, tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        col[(size_t)(t + R1 * r) * N] = v[r];
+}
+
+// ---- row pass: FFT -> metrics -> amplitude replacement -> IFFT ------------------------------------
+enum GsRowMode : int { GS_FUSED = 0, GS_LAST = 1, GS_STEP = 2 };
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(GsRowCfg<N>::THREADS)
+gs_rows_kernel(const float2 *__restrict__ tw, float2 *__restrict__ state, const float *__restrict__ T, holo_region om, float *__restrict__ inten,
+               float2 *__restrict__ r_out, double *__restrict__ parts, size_t frame_stride_parts)
+{
+    using P = fft::Plan<N>;
+    using C = GsRowCfg<N>;
+    constexpr int R1 = P::R1, E = P::E, RPC = C::RPC;
+    extern __shared__ float2 smem[];
+    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
+    const int fr = blockIdx.x / C::NBLK, blk = blockIdx.x % C::NBLK;
+    const int y = blk * RPC + lr;
+    const size_t rofs = ((size_t)fr * N + y) * N;
+    const float *Ty = T + rofs;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+        v[m] = state[rofs + t + R1 * m];
+    fft::fft2pass<N, false, 1>(v, smem + lr * P::SMEM, t, tw);   // X = N R'_k
+    constexpr float inv_n = 1.0f / (float)N;                 // exact power of two
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int x = t + R1 * r;
+        const float2 X = v[r];
+        const float m2 = X.x * X.x + X.y * X.y;
+        const float I = m2 * (inv_n * inv_n);
+        const float amp = sqrtf(m2) * inv_n;                 // |R'_k|
+        const float tt = __ldg(Ty + x);
+        const float d = amp - tt;
+        s[3] += (double)(d * d);
+        if (in_region(y, x, om)) {
+            const double Id = I, t2 = (double)tt * tt;
+            s[0] += Id;
+            s[1] += Id * Id;
+            s[2] += Id * t2;
+        }
+        if (MODE == GS_LAST || MODE == GS_STEP) {
+            if (inten != nullptr)
+                inten[rofs + x] = I;
+        }
+        if (MODE != GS_LAST) {
+            float2 R;
+            if (m2 > 0.0f) {
+                const float sc = tt * rsqrtf(m2);
+                R = make_float2(X.x * sc, X.y * sc);
+            } else {
+                R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
+            }
+            v[r] = R;
+        }
+    }
+    block_reduce_n(s, 4, parts + (size_t)fr * frame_stride_parts + (size_t)blk * 4);
+    if (MODE == GS_STEP) {
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            r_out[rofs + t + R1 * r] = v[r];
+    } else if (MODE == GS_FUSED) {
+        fft::fft2pass<N, true, 1>(v, smem + lr * P::SMEM, t, tw);
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            state[rofs + t + R1 * r] = v[r];
+    }
+}
+
+// One CTA per (frame, iteration): fixed-order sums -> MSE (R-12) and E.
+__global__ void __launch_bounds__(128)
+gs_mse_kernel(const double *__restrict__ parts, const double *__restrict__ tparts, int nblk, int iters,
+              double inv_count, double *__restrict__ mse, double *__restrict__ err_e)
+{
+    const int b = blockIdx.x / iters;
+    const double *p = parts + (size_t)blockIdx.x * nblk * 4;
+    const double *q = tparts + (size_t)b * nblk * 2;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    double u[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+        for (int k = 0; k < 4; ++k)
+            s[k] += p[(size_t)i * 4 + k];
+        u[0] += q[(size_t)i * 2];
+        u[1] += q[(size_t)i * 2 + 1];
+    }
+    __shared__ double o1[4];
+    __shared__ double o2[4];
+    block_reduce_n(s, 4, o1);
+    __syncthreads();
+    block_reduce_n(u, 2, o2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double a = o1[0] == 0.0 ? 0.0 : o2[0] / o1[0];
+        const double sum = a * a * o1[1] - 2.0 * a * o1[2] + o2[1];
+        if (mse)
+            mse[blockIdx.x] = (sum > 0.0 ? sum : 0.0) * inv_count;
+        if (err_e)
+            err_e[blockIdx.x] = o1[3];
+    }
+}
+
+// ---- host orchestration --------------------------------------------------------------------------
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int gs_group(int n, int batch)
+{
+    const size_t frame = (size_t)n * n * sizeof(float2);
+    size_t budget = 32ull << 20;   // state of a group stays L2-resident across iterations
+    if (const char *e = getenv("HOLO_GS_GROUP_BYTES"))
+        budget = strtoull(e, nullptr, 10);
+    long g = (long)(budget / frame);
+    if (g < 1)
+        g = 1;
+    if (g > kMaxGroup)
+        g = kMaxGroup;
+    if (g > batch)
+        g = batch;
+    return (int)g;
+}
+
+static int gs_nblk(int n)
+{
+    switch (n) {
+    case 16: return GsRowCfg<16>::NBLK;
+    case 32: return GsRowCfg<32>::NBLK;
+    case 64: return GsRowCfg<64>::NBLK;
+    case 128: return GsRowCfg<128>::NBLK;
+    case 256: return GsRowCfg<256>::NBLK;
+    case 512: return GsRowCfg<512>::NBLK;
+    case 1024: return GsRowCfg<1024>::NBLK;
+    default: return GsRowCfg<2048>::NBLK;
+    }
+}
+
+struct GsWs {
+    float2 *state;
+    double *parts;
+    double *tparts;
+};
+
+static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
+{
+    const size_t P = (size_t)n * n;
+    const int G = gs_group(n, batch), nblk = gs_nblk(n);
+    size_t off = 0;
+    const size_t o_state = off;
+    off = al256(off + (size_t)G * P * sizeof(float2));
+    const size_t o_parts = off;
+    off = al256(off + (size_t)batch * iters * nblk * 4 * sizeof(double));
+    const size_t o_tparts = off;
+    off = al256(off + (size_t)batch * nblk * 2 * sizeof(double));
+    if (w) {
+        w->state = (float2 *)(base + o_state);
+        w->parts = (double *)(base + o_parts);
+        w->tparts = (double *)(base + o_tparts);
+    }
+    return off;
+}
+
+holo_status check_n(int n);
+holo_status check_region(holo_region om, int n);
+
+static uint32_t frame_base(uint64_t off, uint64_t b, uint64_t P, uint64_t L)
+{
+    if (L == 0)
+        return 0;
+    unsigned __int128 g = (unsigned __int128)off + (unsigned __int128)b * P;
+    return (uint32_t)(g % L);
+}
+
+// Runs `iters` iterations for all frames (gs_generate, r_in == NULL) or one step
+// from r_in (gs_step, iters == 1, r_out != NULL).
+template <int N>
+static holo_status gs_run(const float2 *tw, const float *target, int batch, int iters, const float2 *lut, uint64_t n_lut,
+                          uint64_t phase_offset, int levels, const float2 *r_in, float2 *r_out, float2 *holo,
+                          uint8_t *holo_levels, float *intensity, double *mse, double *err_e, holo_region om,
+                          void *ws, cudaStream_t s)
+{
+    using RC = GsRowCfg<N>;
+    using CC = GsColCfg<N>;
+    constexpr size_t P = (size_t)N * N;
+    GsWs w;
+    gs_ws_layout(N, batch, iters, (char *)ws, &w);
+    const int G = gs_group(N, batch);
+    const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
+    const size_t pstride = (size_t)iters * RC::NBLK * 4;   // parts per frame
+    for (int g0 = 0; g0 < batch; g0 += G) {
+        const int ng = (batch - g0) < G ? (batch - g0) : G;
+        FrameBases fb;
+        for (int j = 0; j < ng; ++j)
+            fb.b[j] = frame_base(phase_offset, (uint64_t)(g0 + j), P, n_lut);
+        HOLO_TRY(launch(K_GS_ROWS_INIT, gs_rows_init_kernel<N>, dim3(ng * RC::NBLK), dim3(RC::THREADS), RC::SMEM,
+                        s, tw, target + g0 * P, lut, ix, fb, r_in ? r_in + g0 * P : (const float2 *)nullptr, ng, om,
+                        w.state, w.tparts + (size_t)g0 * RC::NBLK * 2));
+        for (int k = 0; k < iters; ++k) {
+            const bool last = (k == iters - 1);
+            HOLO_TRY(launch(K_GS_COLS, gs_cols_kernel<N>, dim3(N / CC::W, ng), dim3(CC::THREADS), CC::SMEM, s,
+                            tw, w.state, levels, (last && holo) ? holo + g0 * P : (float2 *)nullptr,
+                            (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr));
+            double *pk = w.parts + (size_t)g0 * pstride + (size_t)k * RC::NBLK * 4;
+            const float *Tg = target + g0 * P;
+            if (r_out != nullptr) {
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
+                                RC::SMEM, s, tw, w.state, Tg, om, intensity ? intensity + g0 * P : (float *)nullptr,
+                                r_out + g0 * P, pk, pstride));
+            } else if (last) {
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_LAST>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
+                                RC::SMEM, s, tw, w.state, Tg, om, intensity ? intensity + g0 * P : (float *)nullptr,
+                                (float2 *)nullptr, pk, pstride));
+            } else {
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
+                                RC::SMEM, s, tw, w.state, Tg, om, (float *)nullptr, (float2 *)nullptr, pk, pstride));
+            }
+        }
+    }
+    if (mse || err_e) {
+        const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
+        HOLO_TRY(launch(K_MSE_REDUCE, gs_mse_kernel, dim3(batch * iters), dim3(128), 0, s,
+                        (const double *)w.parts, (const double *)w.tparts, RC::NBLK, iters, 1.0 / cnt, mse, err_e));
+    }
+    return HOLO_OK;
+}
+
+static holo_status gs_dispatch(const float2 *tw, int n, const float *target, int batch, int iters, const float2 *lut, uint64_t n_lut,
+                               uint64_t off, int levels, const float2 *r_in, float2 *r_out, float2 *holo,
+                               uint8_t *lev, float *inten, double *mse, double *err_e, holo_region om, void *ws,
+                               cudaStream_t s)
+{
+#define HOLO_GS_CASE(NN)                                                                                  \
+    case NN:                                                                                              \
+        return gs_run<NN>(tw, target, batch, iters, lut, n_lut, off, levels, r_in, r_out, holo, lev, inten,   \
+                          mse, err_e, om, ws, s);
+    switch (n) {
+        HOLO_GS_CASE(16)
+        HOLO_GS_CASE(32)
+        HOLO_GS_CASE(64)
+        HOLO_GS_CASE(128)
+        HOLO_GS_CASE(256)
+        HOLO_GS_CASE(512)
+        HOLO_GS_CASE(1024)
+        HOLO_GS_CASE(2048)
+    default:
+        return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
+    }
+#undef HOLO_GS_CASE
+}
+
+} // namespace holo
+
+using namespace holo;
+
+extern "C" size_t holo_gs_workspace_size(int32_t n, int32_t batch, int32_t iters)
+{
+    if (check_n(n) != HOLO_OK || batch < 1 || iters < 1)
+        return 0;
+    return gs_ws_layout(n, batch, iters, nullptr, nullptr);
+}
+
+static holo_status gs_check_common(const float *target, int32_t n, int32_t batch, int32_t levels, holo_region om,
+                                   uint8_t *holo_levels)
+{
+    HOLO_TRY(check_n(n));
+    HOLO_CHECK_ARG(target != nullptr, "target is NULL");
+    HOLO_CHECK_ARG(batch >= 1, "batch must be >= 1");
+    if (levels < 0 || levels == 1 || levels > 65535)
+        return set_error(HOLO_ERR_UNSUPPORTED, "levels must be 0 or in [2, 65535], got %d", levels);
+    HOLO_CHECK_ARG(holo_levels == nullptr || (levels >= 2 && levels <= 256),
+                   "holo_levels needs 2 <= levels <= 256");
+    HOLO_TRY(check_region(om, n));
+    return HOLO_OK;
+}
+
+extern "C" holo_status holo_gs_generate(const float *target, int32_t n, int32_t batch, int32_t iters,
+                                        const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset, int32_t levels,
+                                        holo_c64 *holo, uint8_t *holo_levels, float *intensity, double *mse,
+                                        double *err_e, holo_region omega, void *ws, size_t ws_bytes,
+                                        holo_stream stream)
+{
+    HOLO_TRY(gs_check_common(target, n, batch, levels, omega, holo_levels));
+    HOLO_CHECK_ARG(iters >= 1, "iters must be >= 1");
+    HOLO_CHECK_ARG(n_lut < (1ull << 31), "n_lut must be < 2^31");
+    HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
+    HOLO_CHECK_ARG(ws != nullptr, "workspace is NULL");
+    const size_t need = holo_gs_workspace_size(n, batch, iters);
+    if (ws_bytes < need)
+        return set_error(HOLO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    const float2 *tw = nullptr;
+    HOLO_TRY(fft::twiddles(&tw));
+    return gs_dispatch(tw, n, target, batch, iters, (const float2 *)lut, n_lut, phase_offset, levels, nullptr, nullptr,
+                       (float2 *)holo, holo_levels, intensity, mse, err_e, omega, ws, (cudaStream_t)stream);
+}
+
+extern "C" holo_status holo_gs_step(const holo_c64 *r_in, const float *target, int32_t n, int32_t batch,
+                                    int32_t levels, holo_c64 *r_out, holo_c64 *holo, uint8_t *holo_levels,
+                                    float *intensity, double *mse, double *err_e, holo_region omega, void *ws,
+                                    size_t ws_bytes, holo_stream stream)
+{
+    HOLO_TRY(gs_check_common(target, n, batch, levels, omega, holo_levels));
+    HOLO_CHECK_ARG(r_in != nullptr && r_out != nullptr, "r_in and r_out are required");
+    HOLO_CHECK_ARG((const void *)r_in != (const void *)r_out, "r_in and r_out must not alias");
+    HOLO_CHECK_ARG(ws != nullptr, "workspace is NULL");
+    const size_t need = holo_gs_workspace_size(n, batch, 1);
+    if (ws_bytes < need)
+        return set_error(HOLO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    const float2 *tw = nullptr;
+    HOLO_TRY(fft::twiddles(&tw));
+    return gs_dispatch(tw, n, target, batch, 1, nullptr, 0, 0, levels, (const float2 *)r_in, (float2 *)r_out,
+                       (float2 *)holo, holo_levels, intensity, mse, err_e, omega, ws, (cudaStream_t)stream);
+}

@@ -1,0 +1,140 @@
+// hooks.cu -- test hooks of the C ABI (not on the hot path): a plain unitary 2D
+// DFT/IDFT (Eqs. (1)-(2)) built from the same FFT device code as the
+// fused passes, and step a2 (randomisation) alone for bit-exact probing.
+#include "fft.cuh"
+
+namespace holo {
+
+template <int N>
+struct HookRowCfg {
+    using P = fft::Plan<N>;
+    static constexpr int RPC = (N >= 2048) ? 4 : ((256 / P::T) < N ? (256 / P::T) : N);
+    static constexpr int THREADS = RPC * P::T;
+    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
+};
+
+template <int N>
+struct HookColCfg {
+    using P = fft::Plan<N>;
+    static constexpr int W = 8;
+    static constexpr int THREADS = W * P::T;
+    static constexpr size_t SMEM = (size_t)W * P::SMEM * sizeof(float2);
+};
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(HookRowCfg<N>::THREADS)
+fft_rows_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ in, float2 *__restrict__ out, int nrows)
+{
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E, RPC = HookRowCfg<N>::RPC;
+    extern __shared__ float2 smem[];
+    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
+    const int g = blockIdx.x * RPC + lr;
+    const bool active = g < nrows;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+        v[m] = active ? in[(size_t)g * N + t + R1 * m] : make_float2(0.f, 0.f);
+    fft::fft2pass<N, INV, 1>(v, smem + lr * P::SMEM, t, tw);
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            out[(size_t)g * N + t + R1 * r] = v[r];
+    }
+}
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(HookColCfg<N>::THREADS) fft_cols_kernel(const float2 *__restrict__ tw, float2 *__restrict__ buf, float scale)
+{
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E, W = HookColCfg<N>::W;
+    extern __shared__ float2 smem[];
+    const int c = threadIdx.x % W, t = threadIdx.x / W;
+    float2 *col = buf + (size_t)blockIdx.y * N * N + blockIdx.x * W + c;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+        v[m] = col[(size_t)(t + R1 * m) * N];
+    fft::fft2pass<N, INV, W>(v, smem + c, t, tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        col[(size_t)(t + R1 * r) * N] = make_float2(v[r].x * scale, v[r].y * scale);
+}
+
+template <int N>
+static holo_status fft2_run(const float2 *tw, const float2 *in, float2 *out, int batch, int inverse, cudaStream_t s)
+{
+    using RC = HookRowCfg<N>;
+    using CC = HookColCfg<N>;
+    const int nrows = batch * N;
+    const dim3 rg((nrows + RC::RPC - 1) / RC::RPC), cg(N / CC::W, batch);
+    const float scale = 1.0f / (float)N;   // unitary: 1/sqrt(N*N), an exact power of two
+    if (inverse) {
+        HOLO_TRY(launch(K_FFT_ROWS, fft_rows_kernel<N, true>, rg, dim3(RC::THREADS), RC::SMEM, s, tw, in, out, nrows));
+        HOLO_TRY(launch(K_FFT_COLS, fft_cols_kernel<N, true>, cg, dim3(CC::THREADS), CC::SMEM, s, tw, out, scale));
+    } else {
+        HOLO_TRY(launch(K_FFT_ROWS, fft_rows_kernel<N, false>, rg, dim3(RC::THREADS), RC::SMEM, s, tw, in, out, nrows));
+        HOLO_TRY(launch(K_FFT_COLS, fft_cols_kernel<N, false>, cg, dim3(CC::THREADS), CC::SMEM, s, tw, out, scale));
+    }
+    return HOLO_OK;
+}
+
+__global__ void __launch_bounds__(256)
+randomise_kernel(const float *__restrict__ T, int P, const float2 *__restrict__ lut, LutIndexer ix, uint32_t base,
+                 float2 *__restrict__ r_out)
+{
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+        const float t = T[p];
+        if (lut == nullptr) {
+            r_out[p] = make_float2(t, 0.0f);
+        } else {
+            const float2 c = lut_at(lut, ix.mod_any((uint64_t)base + (uint64_t)p));
+            r_out[p] = make_float2(t * c.x, t * c.y);   // a2, fp32 products
+        }
+    }
+}
+
+holo_status check_n(int n);
+
+} // namespace holo
+
+using namespace holo;
+
+extern "C" holo_status holo_fft2(const holo_c64 *in, holo_c64 *out, int32_t n, int32_t batch, int32_t inverse,
+                                 holo_stream stream)
+{
+    HOLO_TRY(check_n(n));
+    HOLO_CHECK_ARG(in != nullptr && out != nullptr, "in/out is NULL");
+    HOLO_CHECK_ARG(batch >= 1, "batch must be >= 1");
+    const float2 *tw = nullptr;
+    HOLO_TRY(fft::twiddles(&tw));
+    const float2 *i = (const float2 *)in;
+    float2 *o = (float2 *)out;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (n) {
+    case 16: return fft2_run<16>(tw, i, o, batch, inverse, s);
+    case 32: return fft2_run<32>(tw, i, o, batch, inverse, s);
+    case 64: return fft2_run<64>(tw, i, o, batch, inverse, s);
+    case 128: return fft2_run<128>(tw, i, o, batch, inverse, s);
+    case 256: return fft2_run<256>(tw, i, o, batch, inverse, s);
+    case 512: return fft2_run<512>(tw, i, o, batch, inverse, s);
+    case 1024: return fft2_run<1024>(tw, i, o, batch, inverse, s);
+    case 2048: return fft2_run<2048>(tw, i, o, batch, inverse, s);
+    default: return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
+    }
+}
+
+extern "C" holo_status holo_debug_randomise(const float *target, int32_t n, const holo_c64 *lut, uint64_t n_lut,
+                                            uint64_t offset, holo_c64 *r_out, holo_stream stream)
+{
+    HOLO_TRY(check_n(n));
+    HOLO_CHECK_ARG(target != nullptr && r_out != nullptr, "target/r_out is NULL");
+    HOLO_CHECK_ARG(n_lut < (1ull << 31), "n_lut must be < 2^31");
+    HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
+    const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, n);
+    const uint32_t base = n_lut ? (uint32_t)(offset % n_lut) : 0u;
+    const int P = n * n;
+    const int grid = (P + 255) / 256 < 1184 ? (P + 255) / 256 : 1184;
+    return launch(K_RANDOMISE, randomise_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, target, P,
+                  (const float2 *)lut, ix, base, (float2 *)r_out);
+}

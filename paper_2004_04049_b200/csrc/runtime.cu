@@ -1,0 +1,213 @@
+// runtime.cu -- libholo host runtime: status strings, launch accounting,
+// event-based kernel profiling, per-device twiddle tables, version.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <map>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace holo {
+
+const char *const kKernelNames[K_NUM_KERNELS] = {
+    "lut_generate", "ospr_rows_a", "ospr_cols", "ospr_rows_c", "ospr_finalize", "mse_reduce",
+    "gs_rows_init", "gs_cols",     "gs_rows",   "fft_rows",    "fft_cols",      "randomise",
+};
+
+static thread_local std::string t_error;
+
+holo_status set_error(holo_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_error = buf;
+    return st;
+}
+
+holo_status cuda_status(cudaError_t e, const char *where)
+{
+    return set_error(HOLO_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// ---- launch accounting and profiling -------------------------------------------------------
+static std::atomic<uint64_t> g_launches{0};
+static std::mutex g_prof_mu;
+static std::atomic<bool> g_prof_on{false};
+struct ProfRec {
+    int id;
+    cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_event_pool;
+static thread_local cudaEvent_t t_pending = nullptr;
+
+static cudaEvent_t take_event()
+{
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void prof_before(KernelId id, cudaStream_t s)
+{
+    (void)id;
+    if (!g_prof_on.load(std::memory_order_relaxed))
+        return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    t_pending = take_event();
+    cudaEventRecord(t_pending, s);
+}
+
+void prof_after(KernelId id, cudaStream_t s)
+{
+    if (!g_prof_on.load(std::memory_order_relaxed) || t_pending == nullptr)
+        return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, s);
+    g_recs.push_back(ProfRec{(int)id, t_pending, b});
+    t_pending = nullptr;
+}
+
+static std::mutex g_smem_mu;
+static std::set<std::pair<int, const void *>> g_smem_done;
+
+holo_status ensure_smem(const void *fn, size_t smem)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    auto key = std::make_pair(dev, fn);
+    if (g_smem_done.count(key))
+        return HOLO_OK;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    g_smem_done.insert(key);
+    return HOLO_OK;
+}
+
+namespace fft {
+
+static std::mutex g_tw_mu;
+static std::map<int, float2 *> g_tw_dev;
+
+holo_status twiddles(const float2 **pool)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(g_tw_mu);
+    auto it = g_tw_dev.find(dev);
+    if (it != g_tw_dev.end()) {
+        *pool = it->second;
+        return HOLO_OK;
+    }
+    std::vector<float2> host(kTwPool, make_float2(0.f, 0.f));
+    for (int lg = 4; lg <= 11; ++lg) {
+        int n = 1 << lg, r1 = 1 << (lg / 2), r2 = n / r1, off = n - 16;
+        for (int r = 0; r < r2; ++r)
+            for (int t = 0; t < r1; ++t) {
+                long long m = ((long long)r * t) % n;
+                double a = -2.0 * 3.14159265358979323846 * (double)m / (double)n;
+                host[off + r * r1 + t] = make_float2((float)std::cos(a), (float)std::sin(a));
+            }
+    }
+    float2 *d = nullptr;
+    e = cudaMalloc(&d, sizeof(float2) * kTwPool);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaMalloc(twiddles)");
+    e = cudaMemcpy(d, host.data(), sizeof(float2) * kTwPool, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaMemcpy(twiddles)");
+    g_tw_dev[dev] = d;
+    *pool = d;
+    return HOLO_OK;
+}
+
+} // namespace fft
+} // namespace holo
+
+using namespace holo;
+
+extern "C" const char *holo_last_error(void) { return t_error.c_str(); }
+
+extern "C" const char *holo_version(void) { return "holo 0.1.0 sm_100a"; }
+
+extern "C" uint64_t holo_launch_count(void) { return g_launches.load(); }
+
+extern "C" holo_status holo_profile_enable(int32_t on)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (on) {
+        for (auto &r : g_recs) {
+            cudaEventSynchronize(r.b);
+            g_event_pool.push_back(r.a);
+            g_event_pool.push_back(r.b);
+        }
+        g_recs.clear();
+    }
+    g_prof_on.store(on != 0);
+    return HOLO_OK;
+}
+
+extern "C" holo_status holo_profile_read(const char *name, uint64_t *launches, double *total_ms)
+{
+    int id = -1;
+    for (int k = 0; k < K_NUM_KERNELS; ++k)
+        if (name && std::string(name) == kKernelNames[k])
+            id = k;
+    if (id < 0)
+        return set_error(HOLO_ERR_INVALID_ARG, "unknown kernel name '%s'", name ? name : "(null)");
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    uint64_t n = 0;
+    double ms = 0.0;
+    for (auto &r : g_recs) {
+        if (r.id != id)
+            continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess)
+            return cuda_status(e, "cudaEventSynchronize");
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms += t;
+        ++n;
+    }
+    if (launches)
+        *launches = n;
+    if (total_ms)
+        *total_ms = ms;
+    return HOLO_OK;
+}
+
+extern "C" const char *holo_kernel_names(void)
+{
+    static std::string s;
+    static std::once_flag f;
+    std::call_once(f, [] {
+        for (int k = 0; k < K_NUM_KERNELS; ++k) {
+            if (k)
+                s += ",";
+            s += kKernelNames[k];
+        }
+    });
+    return s.c_str();
+}

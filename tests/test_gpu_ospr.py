@@ -1,0 +1,218 @@
+"""GPU parity of the OSPR path (steps a0-a7) against the fp64 oracle.
+
+Protocol: P-1 LUT bit-exact; P-2 randomisation bit-exact; P-3
+bits exact outside the |Re H| < 1e-5 max band; P-4 intensity conditional on
+the GPU's bits, rel 1e-4; P-5 MSE unconditional, rel 1e-4; P-8 shards
+reproduce the single call; P-9 LUT lengths beyond the BASELINE ones.
+All calls go through the C ABI (paper_2004_04049_b200 -> libholo.so).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from holo_synth import LUT_SEED, WORKLOADS, Region, blobs_target, p9_lengths, target_for
+from parity import (REL_TOL, check_bits, check_intensity, cuda_target, lut_pair, rel, to_np, unpack)
+
+pytestmark = pytest.mark.gpu
+
+hb = pytest.importorskip("paper_2004_04049_b200")
+
+
+# ---- P-1 / P-2 ----------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("L", [1, 5, 256, 4096, 10007, 1 << 16, 1 << 20, 1024 * 1024 * 24])
+def test_lut_bit_exact(L):
+    g = to_np(torch.view_as_real(hb.lut_generate(LUT_SEED, L)).contiguous())
+    o = oracle.lut_build(LUT_SEED, L)
+    assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+def test_lut_other_seeds_and_prefix():
+    for seed in (0, 1, 2 ** 63 + 17):
+        g = to_np(torch.view_as_real(hb.lut_generate(seed, 3001)).contiguous())
+        assert np.array_equal(g.view(np.uint32), oracle.lut_build(seed, 3001).view(np.uint32))
+    a = hb.lut_generate(9, 1000)
+    b = hb.lut_generate(9, 70001)
+    assert torch.equal(a, b[:1000])
+
+
+@pytest.mark.parametrize("L", [0, 1, 5, 13, 256, 257, 1021, 10007, 65, 4097])
+@pytest.mark.parametrize("offset", [0, 12345, (1 << 33) + 7])
+def test_randomise_bit_exact(L, offset):
+    n = 64
+    T = target_for(WORKLOADS["C1"])
+    lg, lo = lut_pair(LUT_SEED, L)
+    R = to_np(hb.debug_randomise(cuda_target(T), lg, offset))
+    ref = oracle.apply_phase(T, lo, offset).astype(np.complex64)
+    assert np.array_equal(R.view(np.uint32), ref.view(np.uint32))
+
+
+# ---- unitary DFT hook ------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_fft2_matches_oracle(n, inverse):
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal((2, n, n)) + 1j * rng.standard_normal((2, n, n))).astype(np.complex64)
+    y = to_np(hb.fft2(torch.from_numpy(x).cuda(), inverse=inverse))
+    for b in range(2):
+        ref = oracle.fft2(x[b].astype(np.complex128), inverse)
+        d = y[b] - ref
+        assert np.linalg.norm(d) / np.linalg.norm(ref) <= 1e-6
+        assert np.max(np.abs(d)) <= 1e-5 * np.max(np.abs(ref))
+
+
+# ---- OSPR end to end -----------------------------------------------------------------------------------
+
+def ospr_parity(T, n_sub, L, offset=0, region=None, frames_T=None):
+    """Run GPU OSPR and check P-3/P-4/P-5 for every sub-frame of every frame."""
+    Ts = np.stack(frames_T) if frames_T is not None else T[None]
+    F, n, _ = Ts.shape
+    region = region or Region.upper_half(n).as_tuple()
+    lg, lo = lut_pair(LUT_SEED, L)
+    res = hb.ospr_generate(cuda_target(Ts), n_sub, lg, phase_offset=offset, omega=region)
+    bits, I, mse = to_np(res.bits), to_np(res.intensity), to_np(res.mse)
+    P = n * n
+    flips = exempt = 0
+    for f in range(F):
+        for s in range(n_sub):
+            _, h_re, _ = oracle.ospr_subframe(Ts[f], lo, offset + (f * n_sub + s) * P, want_h=True,
+                                              want_intensity=False)
+            e, fl = check_bits(bits[f, s], h_re, n)
+            exempt += e
+            flips += fl
+        I_cond = oracle.replay_from_bits(bits[f], n)              # P-4: oracle propagates GPU bits
+        check_intensity(I[f], I_cond)
+    _, I_ref, mse_ref = oracle.ospr(Ts, n_sub, lo, offset, region)
+    for f in range(F):
+        assert rel(mse[f], mse_ref[f]) <= REL_TOL, (f, mse[f], mse_ref[f])   # P-5
+    return res, flips, exempt
+
+
+@pytest.mark.parametrize("L", [256] + list(p9_lengths(64)))
+def test_ospr_c1_all_lengths(L):
+    """BASELINE configs[0] (64x64, N_SF = 8, L = 256) plus the P-9 lengths."""
+    w = WORKLOADS["C1"]
+    ospr_parity(target_for(w), w.n_sub, L)
+
+
+@pytest.mark.parametrize("offset", [1, 777, (1 << 35) + 3])
+def test_ospr_phase_offset(offset):
+    ospr_parity(target_for(WORKLOADS["C1"]), 8, 1021, offset=offset)
+
+
+def test_ospr_odd_subframes_multi_frame():
+    """Odd N_SF leaves an unpaired sub-frame; frames continue the cursor."""
+    n = 64
+    Ts = [blobs_target(40 + f, n, 4, 4.0, 10.0, Region.upper_half(n)) for f in range(3)]
+    ospr_parity(None, 5, 1021, offset=99, frames_T=Ts)
+
+
+@pytest.mark.parametrize("n", [16, 32, 128, 256, 512])
+def test_ospr_sizes(n):
+    T = blobs_target(7, n, 4, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n))
+    ospr_parity(T, 3, 10007)
+
+
+def test_ospr_single_subframe_and_flat():
+    T = target_for(WORKLOADS["C1"])
+    ospr_parity(T, 1, 257)
+    res, _, _ = ospr_parity(T, 4, 0)           # flat: all sub-frames identical
+    b = to_np(res.bits)[0]
+    assert all(np.array_equal(b[0], b[s]) for s in range(4))
+
+
+def test_ospr_shards_reproduce_single_call():
+    """P-8 on one GPU: shard ranges with global draw indices give bit-identical
+    holograms, and finalize(sum of partial sums) matches the single call."""
+    n, S = 64, 7
+    T = target_for(WORKLOADS["C1"])
+    tg = cuda_target(T)
+    lut = hb.lut_generate(LUT_SEED, 1021)
+    full = hb.ospr_generate(tg, S, lut, phase_offset=5)
+    parts = [(0, 3), (3, 4), (4, 7)]
+    acc = torch.zeros_like(full.intensity)
+    for b, e in parts:
+        r = hb.ospr_generate(tg, S, lut, phase_offset=5, sf_range=(b, e))
+        assert r.mse is None
+        assert torch.equal(r.bits, full.bits[:, b:e])
+        acc += r.intensity
+    mean, mse = hb.ospr_finalize(tg, acc, S)
+    d = (mean - full.intensity).abs().max().item() / full.intensity.abs().max().item()
+    assert d <= 1e-6
+    assert rel(mse.item(), full.mse.item()) <= 1e-5
+
+
+def test_ospr_deterministic():
+    T = cuda_target(target_for(WORKLOADS["C1"]))
+    lut = hb.lut_generate(LUT_SEED, 257)
+    a = hb.ospr_generate(T, 8, lut)
+    b = hb.ospr_generate(T, 8, lut)
+    assert torch.equal(a.bits, b.bits) and torch.equal(a.intensity, b.intensity) and torch.equal(a.mse, b.mse)
+
+
+def test_ospr_properties():
+    """Energy (Parseval, sum I = N^2), conjugate symmetry and the DC closed form on the
+    GPU output alone."""
+    n, S = 128, 6
+    T = blobs_target(3, n, 8, 4.0, 12.0, Region.upper_half(n))
+    res = hb.ospr_generate(cuda_target(T), S, hb.lut_generate(LUT_SEED, 10007))
+    I = to_np(res.intensity)[0].astype(np.float64)
+    assert abs(I.sum() - n * n) <= 1e-5 * n * n
+    mirror = np.roll(np.flip(I, (0, 1)), 1, axis=(0, 1))
+    assert np.max(np.abs(I - mirror)) <= 1e-6 * I.max()
+    pops = unpack(to_np(res.bits)[0], n).reshape(S, -1).sum(1).astype(np.float64)
+    dc = np.mean((2 * pops - n * n) ** 2 / (n * n))
+    assert abs(I[0, 0] - dc) <= 1e-5 * max(dc, 1.0)
+
+
+# ---- BASELINE full-size configurations ------------------------------------------------------------------
+
+@pytest.mark.parametrize("L", [1 << 16, 1024 * 1024 * 24])
+def test_ospr_c3_full_parity(L):
+    """BASELINE configs[2] at full size (1024^2, N_SF = 24) in the bench's launch
+    configuration: every sub-frame's bits, conditional intensity and MSE."""
+    w = WORKLOADS["C3"]
+    _, flips, exempt = ospr_parity(target_for(w), w.n_sub, L)
+    assert flips <= exempt
+
+
+@pytest.mark.parametrize("L", [1 << 8, 1 << 12, 1 << 20])
+def test_ospr_c3_sampled_and_degenerate(L):
+    """The other C3 lengths all divide N^2 (pin c3 #13): on the GPU every sub-frame must
+    come out bit-identical; sub-frame 0 is checked against the oracle; MSE of the mean
+    equals the oracle's single-sub-frame MSE."""
+    w = WORKLOADS["C3"]
+    T = target_for(w)
+    lg, lo = lut_pair(LUT_SEED, L)
+    res = hb.ospr_generate(cuda_target(T), w.n_sub, lg)
+    bits = to_np(res.bits)[0]
+    assert all(np.array_equal(bits[0], bits[s]) for s in range(w.n_sub))
+    _, h_re, I1 = oracle.ospr_subframe(T, lo, 0, want_h=True, want_intensity=True)
+    check_bits(bits[0], h_re, w.n)
+    check_intensity(to_np(res.intensity)[0], oracle.replay_from_bits(bits[:1], w.n))
+    m_ref = oracle.mse_m1(I1, T, w.omega().as_tuple())
+    assert rel(to_np(res.mse)[0], m_ref) <= REL_TOL
+
+
+def test_ospr_c5_sampled():
+    """BASELINE configs[4] shape (2048^2, N_SF = 32, L = 2^16), two frames.  L divides
+    N^2 (pin c3 #13), so every sub-frame of a frame must be bit-identical on the GPU;
+    sampled sub-frames (incl. frame 1, cursor f N_SF N^2) are checked against the oracle
+    and each frame's MSE against the oracle's single-sub-frame MSE (equal by the
+    degeneracy)."""
+    w = WORKLOADS["C5"]
+    Ts = np.stack([target_for(w, f) for f in range(2)])
+    lg, lo = lut_pair(LUT_SEED, 1 << 16)
+    res = hb.ospr_generate(cuda_target(Ts), w.n_sub, lg)
+    bits, I, mse = to_np(res.bits), to_np(res.intensity), to_np(res.mse)
+    n, P = w.n, w.n * w.n
+    for f in range(2):
+        assert all(np.array_equal(bits[f, 0], bits[f, s]) for s in range(w.n_sub))
+    for f, s in [(0, 0), (0, 31), (1, 0)]:
+        _, h_re, I1 = oracle.ospr_subframe(Ts[f], lo, (f * w.n_sub + s) * P, want_h=True, want_intensity=True)
+        check_bits(bits[f, s], h_re, n)
+        if s == 0:
+            assert rel(mse[f], oracle.mse_m1(I1, Ts[f], w.omega().as_tuple())) <= REL_TOL
+            check_intensity(I[f], oracle.replay_from_bits(bits[f, :1], n))
