@@ -30,7 +30,8 @@ holo_status cuda_status(cudaError_t e, const char *where);
 // ---- kernel classes (profiling names) ----------------------------------------------------
 enum KernelId : int {
     K_LUT_GENERATE = 0,
-    K_OSPR_ROWS_A,      // prologue (T x LUT, Hermitian pairing) + row IFFT
+    K_OSPR_RANDOMISE,   // T x LUT for a sub-frame pair, Hermitian pairing (streaming)
+    K_OSPR_ROWS_A,      // row IFFT
     K_OSPR_COLS,        // column IFFT + sign quantise + bit pack + column FFT
     K_OSPR_ROWS_C,      // row FFT + |.|^2 accumulate over the chunk's pairs
     K_OSPR_FINALIZE,    // symmetrise/scale + MSE partial sums
@@ -91,15 +92,13 @@ struct LutIndexer {
     {
         LutIndexer r;
         r.L = L;
-        r.M = 0;
+        r.M = (L & (L - 1)) ? UINT64_MAX / L + 1 : 0;   // Lemire constant (non-powers of two)
         if (L >= n)
             r.mode = 0;
         else if ((L & (L - 1)) == 0)
             r.mode = 1;
-        else {
+        else
             r.mode = 2;
-            r.M = UINT64_MAX / L + 1;
-        }
         return r;
     }
     __device__ __forceinline__ uint32_t mod(uint32_t a) const

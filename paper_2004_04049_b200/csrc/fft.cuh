@@ -189,19 +189,60 @@ holo_status twiddles(const float2 **pool);
 
 __device__ __forceinline__ int pad_index(int i, int r1) { return i + i / r1; }
 
+// Read-only load the compiler may neither hoist nor merge with an earlier load of the same
+// address: keeps two transforms in one kernel from pinning the 2*(R2-1) twiddle registers
+// of the first across the work in between (register pressure -> occupancy).
+__device__ __forceinline__ float2 ldg_nocse(const float2 *p)
+{
+    float2 v;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
+// The R2 pass-2 twiddles W_N^{r*t} (forward sign) of transform role t.  REG = true keeps
+// them in registers across every transform a thread performs with that role (2*(R2-1)
+// registers); REG = false re-reads them from the L1-resident pool per transform.
+template <int N, bool REG = (Plan<N>::E <= 32)>
+struct Twiddles {
+    float2 w[REG ? Plan<N>::R2 : 1];
+    const float2 *p;
+    __device__ __forceinline__ void load(const float2 *__restrict__ twp, int t)
+    {
+        using P = Plan<N>;
+        p = twp + P::TW_OFFSET + t;
+        if constexpr (REG) {
+#pragma unroll
+            for (int r = 0; r < P::R2; ++r)
+                w[r] = __ldg(p + r * P::R1);
+        }
+    }
+    __device__ __forceinline__ float2 get(int r) const
+    {
+        if constexpr (REG)
+            return w[r];
+        else
+            return ldg_nocse(p + r * Plan<N>::R1);
+    }
+};
+
 // Two-pass FFT of one length-N transform held by T = R1 threads (see header).
 // `sm` points at this transform's exchange buffer (element i at sm[(i + i/R1)*IL]).
-// All threads of the CTA must call this together (it contains __syncthreads()).
-template <int N, bool INV, int IL>
-__device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, int t,
-                                         const float2 *__restrict__ twp)
+// WS = true: the T threads of the transform live in one warp (T <= 32, row kernels)
+// and synchronise with __syncwarp(), so warps run independently; WS = false: the
+// threads span warps (column tiles) and every thread of the CTA must call this
+// together (__syncthreads()).
+template <int N, bool INV, int IL, bool WS, class TwSrc>
+__device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *sm, int t, const TwSrc &tws)
 {
     using P = Plan<N>;
     constexpr int R1 = P::R1, R2 = P::R2, Q = P::Q;
 #pragma unroll
     for (int b = 0; b < Q; ++b)
         Dft<R1, Q, INV>::run(v + b);
-    __syncthreads();                        // previous readers of sm are done
+    if (WS)
+        __syncwarp();
+    else
+        __syncthreads();                    // previous readers of sm are done
 #pragma unroll
     for (int b = 0; b < Q; ++b)
 #pragma unroll
@@ -209,14 +250,16 @@ __device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, in
             const int i = (t + R1 * b) * R1 + r;
             sm[(i + t + R1 * b) * IL] = v[b + Q * r];   // i/R1 == t + R1*b
         }
-    __syncthreads();
-    const float2 *tw = twp + P::TW_OFFSET + t;
+    if (WS)
+        __syncwarp();
+    else
+        __syncthreads();
 #pragma unroll
     for (int r = 0; r < R2; ++r) {
         const int i = t + R1 * r;
         float2 x = sm[(i + r) * IL];                       // i/R1 == r
         if (r > 0) {
-            float2 w = __ldg(tw + r * R1);
+            float2 w = tws(r);
             if (INV)
                 w.y = -w.y;
             x = cmul(x, w);
@@ -224,6 +267,33 @@ __device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, in
         v[r] = x;
     }
     Dft<R2, 1, INV>::run(v);
+}
+
+template <int N>
+struct TwGlobal {
+    const float2 *p;
+    __device__ __forceinline__ float2 operator()(int r) const { return ldg_nocse(p + r * Plan<N>::R1); }
+};
+
+template <int N, bool REG>
+struct TwRegs {
+    const Twiddles<N, REG> &tw;
+    __device__ __forceinline__ float2 operator()(int r) const { return tw.get(r); }
+};
+
+// Twiddles read from the global pool (L1-resident) per transform.
+template <int N, bool INV, int IL, bool WS = false>
+__device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, int t,
+                                         const float2 *__restrict__ twp)
+{
+    fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwGlobal<N>{twp + Plan<N>::TW_OFFSET + t});
+}
+
+// Twiddles prepared by the caller (Twiddles<N>::load once per role).
+template <int N, bool INV, int IL, bool WS = false, bool REG = true>
+__device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, int t, const Twiddles<N, REG> &tw)
+{
+    fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwRegs<N, REG>{tw});
 }
 
 } // namespace fft

@@ -12,7 +12,7 @@
 //
 // The 1/sqrt(N) factors of the inverse transforms are dropped: the constraint
 // and the amplitude replacement are invariant to a positive scale.
-#include "fft.cuh"
+#include "passes.cuh"
 
 namespace holo {
 
@@ -20,24 +20,9 @@ constexpr int kMaxGroup = 16;
 
 template <int N>
 struct GsRowCfg {
-    using P = fft::Plan<N>;
-    static constexpr int RPC = (N >= 2048) ? 4 : ((256 / P::T) < N ? (256 / P::T) : N);
-    static constexpr int THREADS = RPC * P::T;
-    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
-    static constexpr int NBLK = N / RPC;   // CTAs per frame
+    static constexpr int NBLK = N / RowPipe<N>::GPW;   // partial-sum slots per frame and iteration
 };
 
-template <int N>
-struct GsColCfg {
-    using P = fft::Plan<N>;
-    static constexpr int W = 8;
-    static constexpr int THREADS = W * P::T;
-    static constexpr size_t SMEM = (size_t)W * P::SMEM * sizeof(float2);
-};
-
-struct FrameBases {
-    uint32_t b[kMaxGroup];
-};
 
 __device__ __forceinline__ void block_reduce_n(double *s, int nvals, double *dst)
 {
@@ -70,178 +55,219 @@ __device__ __forceinline__ bool in_region(int y, int x, const holo_region &om)
     return y >= om.row0 && y < om.row1 && x >= om.col0 && x < om.col1;
 }
 
-// ---- init: R_0 (or R_in) -> row IFFT ---------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(GsRowCfg<N>::THREADS)
-gs_rows_init_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix, FrameBases fb,
-                    const float2 *__restrict__ r_in, int nframes, holo_region om, float2 *__restrict__ state,
-                    double *__restrict__ tparts)
+// ---- g0: R_0 = T * lut[(base_b + p) mod L] (or a given R_in) -> state; T sums over Omega -----------
+constexpr int kGsTBlocks = 64;   // CTAs per frame of the prepare kernel (fixed => deterministic sums)
+
+__device__ __forceinline__ uint32_t gs_lut_mod(uint32_t a, const LutIndexer &ix)
 {
-    using P = fft::Plan<N>;
-    using C = GsRowCfg<N>;
-    constexpr int R1 = P::R1, E = P::E, RPC = C::RPC;
-    extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
-    const int fr = blockIdx.x / C::NBLK, blk = blockIdx.x % C::NBLK;
-    const int y = blk * RPC + lr;
-    const float *Ty = T + ((size_t)fr * N + y) * N;
-    float2 v[E];
+    return (ix.L & (ix.L - 1)) == 0 ? (a & (ix.L - 1)) : (uint32_t)__umul64hi(ix.M * (uint64_t)a, (uint64_t)ix.L);
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix, uint32_t off_mod,
+                  uint32_t p_mod, uint64_t frame0, const float2 *__restrict__ r_in, holo_region om,
+                  float2 *__restrict__ state, double *__restrict__ tparts)
+{
+    constexpr int P = N * N;
+    const int fr = blockIdx.y;
+    const float *Tf = T + (size_t)fr * P;
+    float2 *S = state + (size_t)fr * P;
+    uint32_t base = 0;
+    if (lut != nullptr)
+        base = (uint32_t)(((uint64_t)off_mod + ((frame0 + fr) % ix.L) * (uint64_t)p_mod) % ix.L);
     double s[2] = {0.0, 0.0};
-    if (r_in != nullptr) {
-        const float2 *Ry = r_in + ((size_t)fr * N + y) * N;
-#pragma unroll
-        for (int m = 0; m < E; ++m)
-            v[m] = Ry[t + R1 * m];
-    } else if (lut != nullptr) {
-        const uint32_t ry = ix.mod_any((uint64_t)fb.b[fr] + (uint64_t)y * N);
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int x = t + R1 * m;
-            const float tt = __ldg(Ty + x);
-            const float2 c = lut_at(lut, ix.mod(ry + x));
-            v[m] = make_float2(tt * c.x, tt * c.y);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+        const float t = __ldg(Tf + p);
+        float2 R;
+        if (r_in != nullptr) {
+            R = r_in[(size_t)fr * P + p];
+        } else if (lut != nullptr) {
+            const float2 c = __ldg(lut + gs_lut_mod(base + (uint32_t)p, ix));
+            R = make_float2(__fmul_rn(t, c.x), __fmul_rn(t, c.y));   // a2, exact fp32 products
+        } else {
+            R = make_float2(t, 0.0f);
         }
-    } else {
-#pragma unroll
-        for (int m = 0; m < E; ++m)
-            v[m] = make_float2(__ldg(Ty + t + R1 * m), 0.0f);
-    }
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int x = t + R1 * m;
+        S[p] = R;
+        const int y = p / N, x = p % N;
         if (in_region(y, x, om)) {
-            const double tt = __ldg(Ty + x), t2 = tt * tt;
+            const double td = t, t2 = td * td;
             s[0] += t2;
             s[1] += t2 * t2;
         }
     }
-    fft::fft2pass<N, true, 1>(v, smem + lr * P::SMEM, t, tw);
-    float2 *out = state + ((size_t)fr * N + y) * N;
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-        out[t + R1 * r] = v[r];
-    block_reduce_n(s, 2, tparts + ((size_t)fr * C::NBLK + blk) * 2);
+    block_reduce_n(s, 2, tparts + ((size_t)fr * kGsTBlocks + blockIdx.x) * 2);
 }
 
-// ---- column pass: IFFT -> constraint -> FFT ----------------------------------------------------
+// ---- column pass: IFFT -> constraint -> FFT (TMA-fed pipeline) ----------------------------------
 template <int N>
-__global__ void __launch_bounds__(GsColCfg<N>::THREADS)
-gs_cols_kernel(const float2 *__restrict__ tw, float2 *__restrict__ state, int levels, float2 *__restrict__ holo, uint8_t *__restrict__ lev)
-{
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, W = GsColCfg<N>::W;
-    extern __shared__ float2 smem[];
-    const int c = threadIdx.x % W, t = threadIdx.x / W;
-    const int tile = blockIdx.x, fr = blockIdx.y;
-    const size_t fofs = (size_t)fr * N * N;
-    float2 *col = state + fofs + tile * W + c;
-    float2 v[E];
+struct GsColBody {
+    struct Args {
+        const float2 *tw;
+        float2 *state;
+        int levels;
+        float2 *holo;
+        uint8_t *lev;
+    };
+    template <class TW>
+    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int fr,
+                                               int tile, const Args &a, const TW &twr)
+    {
+        using P = fft::Plan<N>;
+        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
+        const size_t fofs = (size_t)fr * N * N;
+        fft::fft2pass<N, true, W>(v, sm, t, twr);            // H_k (x N)
+        const int levels = a.levels;
+        const float q_over_2pi = (float)levels * 0.15915494309189533577f;
 #pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = col[(size_t)(t + R1 * m) * N];
-    fft::fft2pass<N, true, W>(v, smem + c, t, tw);            // H_k (x N)
-    const float q_over_2pi = (float)levels * 0.15915494309189533577f;
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const float2 h = v[r];
-        float2 o;
-        int j = 0;
-        if (levels == 0) {
-            const float m2 = h.x * h.x + h.y * h.y;
-            if (m2 == 0.0f) {
-                o = make_float2(1.0f, 0.0f);               // R-16: H = 0 -> +1
+        for (int r = 0; r < E; ++r) {
+            const float2 h = v[r];
+            float2 o;
+            int j = 0;
+            if (levels == 0) {
+                const float m2 = h.x * h.x + h.y * h.y;
+                if (m2 == 0.0f) {
+                    o = make_float2(1.0f, 0.0f);               // R-16: H = 0 -> +1
+                } else {
+                    const float rr = 1.0f / sqrtf(m2);
+                    o = make_float2(h.x * rr, h.y * rr);
+                }
             } else {
-                const float rr = rsqrtf(m2);
-                o = make_float2(h.x * rr, h.y * rr);
+                float th = atan2f(h.y, h.x);
+                if (th < 0.0f)
+                    th += 6.28318530717958647692f;
+                j = (int)floorf(th * q_over_2pi + 0.5f);
+                if (j >= levels)
+                    j -= levels;
+                double sn, cs;
+                sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
+                o = make_float2((float)cs, (float)sn);
             }
-        } else {
-            float th = atan2f(h.y, h.x);
-            if (th < 0.0f)
-                th += 6.28318530717958647692f;
-            j = (int)floorf(th * q_over_2pi + 0.5f);
-            if (j >= levels)
-                j -= levels;
-            double sn, cs;
-            sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
-            o = make_float2((float)cs, (float)sn);
+            const size_t idx = fofs + (size_t)(t + R1 * r) * N + tile * W + c;
+            if (a.holo != nullptr)
+                a.holo[idx] = o;
+            if (a.lev != nullptr)
+                a.lev[idx] = (uint8_t)j;
+            v[r] = o;
         }
-        if (holo != nullptr)
-            holo[fofs + (size_t)(t + R1 * r) * N + tile * W + c] = o;
-        if (lev != nullptr)
-            lev[fofs + (size_t)(t + R1 * r) * N + tile * W + c] = (uint8_t)j;
-        v[r] = o;
-    }
-    fft::fft2pass<N, false, W>(v, smem + c, t, tw);
+        fft::fft2pass<N, false, W>(v, sm, t, twr);
+        float2 *col = a.state + fofs + tile * W + c;
 #pragma unroll
-    for (int r = 0; r < E; ++r)
-        col[(size_t)(t + R1 * r) * N] = v[r];
-}
+        for (int r = 0; r < E; ++r)
+            col[(size_t)(t + R1 * r) * N] = v[r];
+    }
+};
 
-// ---- row pass: FFT -> metrics -> amplitude replacement -> IFFT ------------------------------------
+// ---- row pass: FFT -> metrics -> amplitude replacement -> IFFT (row pipeline) ---------------------
 enum GsRowMode : int { GS_FUSED = 0, GS_LAST = 1, GS_STEP = 2 };
 
+// Items are GPW-row groups of the group's frames (NGRP = N / GPW per frame); each item's
+// fp64 partial sums (I, I^2, I T^2 over Omega; (|R'| - T)^2 over the plane) go to
+// parts[frame * frame_stride + grp * 4] for a fixed-order reduction by gs_mse_kernel.
 template <int N, int MODE>
-__global__ void __launch_bounds__(GsRowCfg<N>::THREADS)
-gs_rows_kernel(const float2 *__restrict__ tw, float2 *__restrict__ state, const float *__restrict__ T, holo_region om, float *__restrict__ inten,
-               float2 *__restrict__ r_out, double *__restrict__ parts, size_t frame_stride_parts)
+__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__restrict__ T, int nitems, holo_region om,
+               float *__restrict__ inten, float2 *__restrict__ r_out, double *__restrict__ parts,
+               size_t frame_stride_parts)
 {
     using P = fft::Plan<N>;
-    using C = GsRowCfg<N>;
-    constexpr int R1 = P::R1, E = P::E, RPC = C::RPC;
-    extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
-    const int fr = blockIdx.x / C::NBLK, blk = blockIdx.x % C::NBLK;
-    const int y = blk * RPC + lr;
-    const size_t rofs = ((size_t)fr * N + y) * N;
-    const float *Ty = T + rofs;
-    float2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = state[rofs + t + R1 * m];
-    fft::fft2pass<N, false, 1>(v, smem + lr * P::SMEM, t, tw);   // X = N R'_k
-    constexpr float inv_n = 1.0f / (float)N;                 // exact power of two
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const int x = t + R1 * r;
-        const float2 X = v[r];
-        const float m2 = X.x * X.x + X.y * X.y;
-        const float I = m2 * (inv_n * inv_n);
-        const float amp = sqrtf(m2) * inv_n;                 // |R'_k|
-        const float tt = __ldg(Ty + x);
-        const float d = amp - tt;
-        s[3] += (double)(d * d);
-        if (in_region(y, x, om)) {
-            const double Id = I, t2 = (double)tt * tt;
-            s[0] += Id;
-            s[1] += Id * Id;
-            s[2] += Id * t2;
-        }
-        if (MODE == GS_LAST || MODE == GS_STEP) {
-            if (inten != nullptr)
-                inten[rofs + x] = I;
-        }
-        if (MODE != GS_LAST) {
-            float2 R;
-            if (m2 > 0.0f) {
-                const float sc = tt * rsqrtf(m2);
-                R = make_float2(X.x * sc, X.y * sc);
-            } else {
-                R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
-            }
-            v[r] = R;
-        }
+    using RP = RowPipe<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const WarpRing ring = make_ring<RP::SLOT_C, RP::WPC>(smem_raw);
+    const int lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    const int stride = gridDim.x * RP::WPC;
+    int item = blockIdx.x * RP::WPC + (threadIdx.x >> 5);
+    if (lane == 0 && item < nitems) {
+        tma::mbar_arrive_expect_tx(&ring.bars[0], RP::IN_BYTES);
+        tma::load_1d(ring.slot(0), state + (size_t)item * GPW * N, RP::IN_BYTES, &ring.bars[0]);
     }
-    block_reduce_n(s, 4, parts + (size_t)fr * frame_stride_parts + (size_t)blk * 4);
-    if (MODE == GS_STEP) {
+    fft::Twiddles<N, false> twr;                          // pool twiddles (register budget)
+    twr.load(tw, t);
+    constexpr float inv_n = 1.0f / (float)N;                 // exact power of two
+    for (int k = 0; item < nitems; item += stride, ++k) {
+        const int s = k & 1;
+        const int nxt = item + stride;
+        if (lane == 0 && nxt < nitems) {
+            tma::mbar_arrive_expect_tx(&ring.bars[s ^ 1], RP::IN_BYTES);
+            tma::load_1d(ring.slot(s ^ 1), state + (size_t)nxt * GPW * N, RP::IN_BYTES, &ring.bars[s ^ 1]);
+        }
+        const int fr = item / NGRP, grp = item % NGRP;
+        const int y = grp * GPW + g;
+        const size_t rofs = ((size_t)fr * N + y) * N;
+        float tv[E];
 #pragma unroll
         for (int r = 0; r < E; ++r)
-            r_out[rofs + t + R1 * r] = v[r];
-    } else if (MODE == GS_FUSED) {
-        fft::fft2pass<N, true, 1>(v, smem + lr * P::SMEM, t, tw);
+            tv[r] = __ldg(T + rofs + t + R1 * r);               // in flight during the FFT
+        tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
+        float2 *sl = reinterpret_cast<float2 *>(ring.slot(s));
+        float2 v[E];
 #pragma unroll
-        for (int r = 0; r < E; ++r)
-            state[rofs + t + R1 * r] = v[r];
+        for (int m = 0; m < E; ++m)
+            v[m] = sl[g * N + t + R1 * m];
+        fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);   // X = N R'_k
+        double sums[4] = {0.0, 0.0, 0.0, 0.0};
+        float fe = 0.0f;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int x = t + R1 * r;
+            const float2 X = v[r];
+            const float m2 = X.x * X.x + X.y * X.y;
+            const float I = m2 * (inv_n * inv_n);
+            const float amp = sqrtf(m2) * inv_n;                 // |R'_k|
+            const float tt = tv[r];
+            const float d = amp - tt;
+            fe += d * d;
+            if (in_region(y, x, om)) {
+                const double Id = I, t2 = (double)tt * tt;
+                sums[0] += Id;
+                sums[1] += Id * Id;
+                sums[2] += Id * t2;
+            }
+            if (MODE == GS_LAST || MODE == GS_STEP) {
+                if (inten != nullptr)
+                    inten[rofs + x] = I;
+            }
+            if (MODE != GS_LAST) {
+                float2 R;
+                if (m2 > 0.0f) {
+                    const float sc = tt / sqrtf(m2);
+                    R = make_float2(__fmul_rn(X.x, sc), __fmul_rn(X.y, sc));   // no contraction into the IFFT
+                } else {
+                    R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
+                }
+                v[r] = R;
+            }
+        }
+        sums[3] = (double)fe;
+        // warp reduction of the item's sums (lanes of all GPW rows of the item)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double x = sums[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                x += __shfl_down_sync(0xffffffffu, x, o);
+            sums[i] = x;
+        }
+        if (lane == 0) {
+            double *dst = parts + (size_t)fr * frame_stride_parts + (size_t)grp * 4;
+            dst[0] = sums[0];
+            dst[1] = sums[1];
+            dst[2] = sums[2];
+            dst[3] = sums[3];
+        }
+        if (MODE == GS_STEP) {
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                r_out[rofs + t + R1 * r] = v[r];
+        } else if (MODE == GS_FUSED) {
+            fft::fft2pass<N, true, 1, true>(v, sl + g * P::SMEM, t, twr);
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                state[rofs + t + R1 * r] = v[r];
+        }
+        tma::fence_proxy_async_smem();
+        __syncwarp();
     }
 }
 
@@ -252,12 +278,13 @@ gs_mse_kernel(const double *__restrict__ parts, const double *__restrict__ tpart
 {
     const int b = blockIdx.x / iters;
     const double *p = parts + (size_t)blockIdx.x * nblk * 4;
-    const double *q = tparts + (size_t)b * nblk * 2;
+    const double *q = tparts + (size_t)b * kGsTBlocks * 2;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     double u[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x)
         for (int k = 0; k < 4; ++k)
             s[k] += p[(size_t)i * 4 + k];
+    for (int i = threadIdx.x; i < kGsTBlocks; i += blockDim.x) {
         u[0] += q[(size_t)i * 2];
         u[1] += q[(size_t)i * 2 + 1];
     }
@@ -326,7 +353,7 @@ static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
     const size_t o_parts = off;
     off = al256(off + (size_t)batch * iters * nblk * 4 * sizeof(double));
     const size_t o_tparts = off;
-    off = al256(off + (size_t)batch * nblk * 2 * sizeof(double));
+    off = al256(off + (size_t)batch * kGsTBlocks * 2 * sizeof(double));
     if (w) {
         w->state = (float2 *)(base + o_state);
         w->parts = (double *)(base + o_parts);
@@ -338,13 +365,6 @@ static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
 holo_status check_n(int n);
 holo_status check_region(holo_region om, int n);
 
-static uint32_t frame_base(uint64_t off, uint64_t b, uint64_t P, uint64_t L)
-{
-    if (L == 0)
-        return 0;
-    unsigned __int128 g = (unsigned __int128)off + (unsigned __int128)b * P;
-    return (uint32_t)(g % L);
-}
 
 // Runs `iters` iterations for all frames (gs_generate, r_in == NULL) or one step
 // from r_in (gs_step, iters == 1, r_out != NULL).
@@ -355,39 +375,44 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                           void *ws, cudaStream_t s)
 {
     using RC = GsRowCfg<N>;
-    using CC = GsColCfg<N>;
     constexpr size_t P = (size_t)N * N;
     GsWs w;
     gs_ws_layout(N, batch, iters, (char *)ws, &w);
     const int G = gs_group(N, batch);
     const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
+    const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
+    const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
     const size_t pstride = (size_t)iters * RC::NBLK * 4;   // parts per frame
     for (int g0 = 0; g0 < batch; g0 += G) {
         const int ng = (batch - g0) < G ? (batch - g0) : G;
-        FrameBases fb;
-        for (int j = 0; j < ng; ++j)
-            fb.b[j] = frame_base(phase_offset, (uint64_t)(g0 + j), P, n_lut);
-        HOLO_TRY(launch(K_GS_ROWS_INIT, gs_rows_init_kernel<N>, dim3(ng * RC::NBLK), dim3(RC::THREADS), RC::SMEM,
-                        s, tw, target + g0 * P, lut, ix, fb, r_in ? r_in + g0 * P : (const float2 *)nullptr, ng, om,
-                        w.state, w.tparts + (size_t)g0 * RC::NBLK * 2));
+        HOLO_TRY(launch(K_GS_ROWS_INIT, gs_prepare_kernel<N>, dim3(kGsTBlocks, ng), dim3(256), 0, s,
+                        target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
+                        r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state,
+                        w.tparts + (size_t)g0 * kGsTBlocks * 2));
+        HOLO_TRY((launch_rows_fft<N, true>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));
         for (int k = 0; k < iters; ++k) {
             const bool last = (k == iters - 1);
-            HOLO_TRY(launch(K_GS_COLS, gs_cols_kernel<N>, dim3(N / CC::W, ng), dim3(CC::THREADS), CC::SMEM, s,
-                            tw, w.state, levels, (last && holo) ? holo + g0 * P : (float2 *)nullptr,
-                            (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr));
+            typename GsColBody<N>::Args ca{tw, w.state, levels, (last && holo) ? holo + g0 * P : (float2 *)nullptr,
+                                           (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr};
+            HOLO_TRY((launch_cols<N, GsColBody<N>>(K_GS_COLS, w.state, ng, ca, s)));
             double *pk = w.parts + (size_t)g0 * pstride + (size_t)k * RC::NBLK * 4;
             const float *Tg = target + g0 * P;
+            using RP = RowPipe<N>;
+            constexpr size_t smem = ring_smem<RP::SLOT_C, RP::WPC>();
+            const int nitems = ng * (N / RP::GPW);
+            float *ig = intensity ? intensity + g0 * P : (float *)nullptr;
             if (r_out != nullptr) {
-                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
-                                RC::SMEM, s, tw, w.state, Tg, om, intensity ? intensity + g0 * P : (float *)nullptr,
-                                r_out + g0 * P, pk, pstride));
+                const int grid = pipe_grid(gs_rows_kernel<N, GS_STEP>, RP::WPC * 32, smem, nitems, RP::WPC);
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                                w.state, Tg, nitems, om, ig, r_out + g0 * P, pk, pstride));
             } else if (last) {
-                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_LAST>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
-                                RC::SMEM, s, tw, w.state, Tg, om, intensity ? intensity + g0 * P : (float *)nullptr,
-                                (float2 *)nullptr, pk, pstride));
+                const int grid = pipe_grid(gs_rows_kernel<N, GS_LAST>, RP::WPC * 32, smem, nitems, RP::WPC);
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_LAST>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                                w.state, Tg, nitems, om, ig, (float2 *)nullptr, pk, pstride));
             } else {
-                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(ng * RC::NBLK), dim3(RC::THREADS),
-                                RC::SMEM, s, tw, w.state, Tg, om, (float *)nullptr, (float2 *)nullptr, pk, pstride));
+                const int grid = pipe_grid(gs_rows_kernel<N, GS_FUSED>, RP::WPC * 32, smem, nitems, RP::WPC);
+                HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                                w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, pk, pstride));
             }
         }
     }

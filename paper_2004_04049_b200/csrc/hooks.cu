@@ -1,80 +1,44 @@
 // hooks.cu -- test hooks of the C ABI (not on the hot path): a plain unitary 2D
 // DFT/IDFT (Eqs. (1)-(2)) built from the same FFT device code as the
 // fused passes, and step a2 (randomisation) alone for bit-exact probing.
-#include "fft.cuh"
+#include "passes.cuh"
 
 namespace holo {
 
-template <int N>
-struct HookRowCfg {
-    using P = fft::Plan<N>;
-    static constexpr int RPC = (N >= 2048) ? 4 : ((256 / P::T) < N ? (256 / P::T) : N);
-    static constexpr int THREADS = RPC * P::T;
-    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
-};
-
-template <int N>
-struct HookColCfg {
-    using P = fft::Plan<N>;
-    static constexpr int W = 8;
-    static constexpr int THREADS = W * P::T;
-    static constexpr size_t SMEM = (size_t)W * P::SMEM * sizeof(float2);
-};
-
 template <int N, bool INV>
-__global__ void __launch_bounds__(HookRowCfg<N>::THREADS)
-fft_rows_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ in, float2 *__restrict__ out, int nrows)
-{
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, RPC = HookRowCfg<N>::RPC;
-    extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
-    const int g = blockIdx.x * RPC + lr;
-    const bool active = g < nrows;
-    float2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = active ? in[(size_t)g * N + t + R1 * m] : make_float2(0.f, 0.f);
-    fft::fft2pass<N, INV, 1>(v, smem + lr * P::SMEM, t, tw);
-    if (active) {
+struct HookColBody {
+    struct Args {
+        const float2 *tw;
+        float2 *buf;
+        float scale;
+    };
+    template <class TW>
+    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int fr,
+                                               int tile, const Args &a, const TW &twr)
+    {
+        using P = fft::Plan<N>;
+        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
+        fft::fft2pass<N, INV, W>(v, sm, t, twr);
+        float2 *col = a.buf + (size_t)fr * N * N + tile * W + c;
 #pragma unroll
         for (int r = 0; r < E; ++r)
-            out[(size_t)g * N + t + R1 * r] = v[r];
+            col[(size_t)(t + R1 * r) * N] = make_float2(v[r].x * a.scale, v[r].y * a.scale);
     }
-}
-
-template <int N, bool INV>
-__global__ void __launch_bounds__(HookColCfg<N>::THREADS) fft_cols_kernel(const float2 *__restrict__ tw, float2 *__restrict__ buf, float scale)
-{
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, W = HookColCfg<N>::W;
-    extern __shared__ float2 smem[];
-    const int c = threadIdx.x % W, t = threadIdx.x / W;
-    float2 *col = buf + (size_t)blockIdx.y * N * N + blockIdx.x * W + c;
-    float2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = col[(size_t)(t + R1 * m) * N];
-    fft::fft2pass<N, INV, W>(v, smem + c, t, tw);
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-        col[(size_t)(t + R1 * r) * N] = make_float2(v[r].x * scale, v[r].y * scale);
-}
+};
 
 template <int N>
 static holo_status fft2_run(const float2 *tw, const float2 *in, float2 *out, int batch, int inverse, cudaStream_t s)
 {
-    using RC = HookRowCfg<N>;
-    using CC = HookColCfg<N>;
     const int nrows = batch * N;
-    const dim3 rg((nrows + RC::RPC - 1) / RC::RPC), cg(N / CC::W, batch);
     const float scale = 1.0f / (float)N;   // unitary: 1/sqrt(N*N), an exact power of two
     if (inverse) {
-        HOLO_TRY(launch(K_FFT_ROWS, fft_rows_kernel<N, true>, rg, dim3(RC::THREADS), RC::SMEM, s, tw, in, out, nrows));
-        HOLO_TRY(launch(K_FFT_COLS, fft_cols_kernel<N, true>, cg, dim3(CC::THREADS), CC::SMEM, s, tw, out, scale));
+        HOLO_TRY((launch_rows_fft<N, true>(K_FFT_ROWS, tw, in, out, nrows, s)));
+        typename HookColBody<N, true>::Args a{tw, out, scale};
+        HOLO_TRY((launch_cols<N, HookColBody<N, true>>(K_FFT_COLS, out, batch, a, s)));
     } else {
-        HOLO_TRY(launch(K_FFT_ROWS, fft_rows_kernel<N, false>, rg, dim3(RC::THREADS), RC::SMEM, s, tw, in, out, nrows));
-        HOLO_TRY(launch(K_FFT_COLS, fft_cols_kernel<N, false>, cg, dim3(CC::THREADS), CC::SMEM, s, tw, out, scale));
+        HOLO_TRY((launch_rows_fft<N, false>(K_FFT_ROWS, tw, in, out, nrows, s)));
+        typename HookColBody<N, false>::Args a{tw, out, scale};
+        HOLO_TRY((launch_cols<N, HookColBody<N, false>>(K_FFT_COLS, out, batch, a, s)));
     }
     return HOLO_OK;
 }

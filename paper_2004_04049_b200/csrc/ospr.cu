@@ -2,11 +2,11 @@
 // steps a1-a7 of DESIGN.md §1) as three fused FFT passes per chunk of
 // sub-frame pairs plus a finalize pass per frame.
 //
-//   pass A  ospr_rows_a  prologue: R_s = T * lut[(base_s + p) mod L] for the two
-//                        sub-frames a, b of a pair at pixels (y, x) and (-y, -x),
-//                        Hermitian parts packed as Z = Herm(R_a) + i Herm(R_b)
-//                        (so F^-1{Z} = Re H_a + i Re H_b);
-//                        row IFFT; write Z (complex64).
+//   pass R  ospr_randomise  R_s = T * lut[(base_s + p) mod L] for the two
+//                        sub-frames a, b of a pair at pixels p and -p, Hermitian
+//                        parts packed as Z = 2 Herm(R_a) + 2i Herm(R_b)
+//                        (so F^-1{Z} = 2 (Re H_a + i Re H_b)).
+//   pass A  ospr_rows_a  row IFFT of Z in place.
 //   pass B  ospr_cols    column IFFT -> H; a4: bit_a = Re H >= 0, bit_b = Im H >= 0,
 //                        packed MSB-first via warp ballots; h' = (+-1) + i(+-1);
 //                        column FFT of h'; write back in place.
@@ -19,170 +19,218 @@
 // All 1/sqrt(N) factors of Eqs. (1)-(2) are dropped inside the passes: a positive
 // scale does not change sign(Re H), and the forward scale 1/N^2 on |X|^2 is an
 // exact power of two applied in pass C.
-#include "fft.cuh"
+#include <type_traits>
+
+#include "passes.cuh"
 
 namespace holo {
 
-constexpr int kMaxChunk = 16;
+constexpr int kMaxChunk = 64;
+
 constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => deterministic sums)
 constexpr int kFinThreads = 256;
 
-template <int N>
-struct RowCfg {
-    using P = fft::Plan<N>;
-    static constexpr int RPC = (N >= 2048) ? 4 : ((256 / P::T) < N ? (256 / P::T) : N);
-    static constexpr int THREADS = RPC * P::T;
-    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
-};
 
-template <int N>
-struct ColCfg {
-    using P = fft::Plan<N>;
-    static constexpr int W = 8;    // columns per CTA = one packed byte per row
-    static constexpr int THREADS = W * P::T;
-    static constexpr size_t SMEM = (size_t)W * P::SMEM * sizeof(float2);
-};
-
-struct PairBases {
-    uint32_t a[kMaxChunk];
-    uint32_t b[kMaxChunk];
-};
-
-// ---- pass A ------------------------------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(RowCfg<N>::THREADS)
-ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix,
-                   PairBases bases, int npairs, int last_has_b, float2 *__restrict__ buf)
+// ---- pass R: randomisation (a1, a2) with Hermitian pairing --------------------------------------
+// Streaming kernel, one thread per unordered pixel pair {(y1, x), (y2, xm)} = {p, -p}
+// of one sub-frame pair (a, b).  T and the LUT are read once per pixel:
+//   Ha = R_a(p) + conj(R_a(-p)) = 2 Herm(R_a)(p),   Hb likewise,   R_s = T * lut[(base_s + p) mod L]
+//   Z(p) = Ha + i Hb,   Z(-p) = conj(Ha) + i conj(Hb)   (the Hermitian parts are conjugate-symmetric)
+// so that F^-1{Z} = 2 (Re H_a + i Re H_b) after pass A.  The pair
+// index space is rows y1 in [1, N/2) x all x, plus x in [0, N/2] of rows 0 and N/2.
+__device__ __forceinline__ uint32_t lut_mod(uint32_t a, const LutIndexer &ix)
 {
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, RPC = RowCfg<N>::RPC;
-    extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
-    const int g = blockIdx.x * RPC + lr;
-    const bool active = g < npairs * N;
-    const int pair = active ? g / N : 0;
-    const int y = g % N, ym = (N - y) & (N - 1);
-    const bool has_b = (pair < npairs - 1) || last_has_b;
-    float2 v[E];
-    if (active) {
-        const float *Ty = T + (size_t)y * N;
-        const float *Tm = T + (size_t)ym * N;
-        if (lut != nullptr) {
-            const uint32_t rya = ix.mod_any((uint64_t)bases.a[pair] + (uint64_t)y * N);
-            const uint32_t rma = ix.mod_any((uint64_t)bases.a[pair] + (uint64_t)ym * N);
-            const uint32_t ryb = ix.mod_any((uint64_t)bases.b[pair] + (uint64_t)y * N);
-            const uint32_t rmb = ix.mod_any((uint64_t)bases.b[pair] + (uint64_t)ym * N);
-#pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const int x = t + R1 * m, xm = (N - x) & (N - 1);
-                const float t1 = __ldg(Ty + x), t2 = __ldg(Tm + xm);
-                const float2 ca1 = lut_at(lut, ix.mod(rya + x));
-                const float2 ca2 = lut_at(lut, ix.mod(rma + xm));
-                // 2 Herm(R_a)[y][x] = R_a[y][x] + conj(R_a[-y][-x])
-                float2 za = make_float2(t1 * ca1.x + t2 * ca2.x, t1 * ca1.y - t2 * ca2.y);
-                float2 zb = make_float2(0.f, 0.f);
-                if (has_b) {
-                    const float2 cb1 = lut_at(lut, ix.mod(ryb + x));
-                    const float2 cb2 = lut_at(lut, ix.mod(rmb + xm));
-                    zb = make_float2(t1 * cb1.x + t2 * cb2.x, t1 * cb1.y - t2 * cb2.y);
-                }
-                v[m] = make_float2(za.x - zb.y, za.y + zb.x);
-            }
-        } else {   // flat phase (N_LUT = 0): R = T, Herm(R) = (T + T(-p)) / 2
-#pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const int x = t + R1 * m, xm = (N - x) & (N - 1);
-                const float h = __ldg(Ty + x) + __ldg(Tm + xm);
-                v[m] = make_float2(h, has_b ? h : 0.f);
+    // any 32-bit a; L a power of two (incl. 1) -> mask, else Lemire's exact fastmod
+    return (ix.L & (ix.L - 1)) == 0 ? (a & (ix.L - 1)) : (uint32_t)__umul64hi(ix.M * (uint64_t)a, (uint64_t)ix.L);
+}
+
+// Draw base of global sub-frame s: (off + s * N^2) mod L with off, N^2 reduced mod L on the
+// host (all operands < 2^31, so the 64-bit product cannot overflow).
+__device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, uint32_t p_mod, uint32_t L)
+{
+    return (uint32_t)(((uint64_t)off_mod + (s % L) * (uint64_t)p_mod) % L);
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+ospr_randomise_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix, uint32_t off_mod,
+                      uint32_t p_mod, uint64_t sf_first, int last_pair_has_b, float2 *__restrict__ buf)
+{
+    constexpr int QFULL = (N / 2 - 1) * N;                // pixel pairs in rows 1 .. N/2-1
+    constexpr int QP = QFULL + 2 * (N / 2 + 1);            // per sub-frame pair
+    const int pair = blockIdx.y;
+    const bool has_b = (pair < (int)gridDim.y - 1) || last_pair_has_b;
+    const bool flat = (lut == nullptr);
+    uint32_t ba = 0, bb = 0;
+    if (!flat) {
+        ba = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair, p_mod, ix.L);
+        bb = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair + 1, p_mod, ix.L);
+    }
+    float2 *Z = buf + (size_t)pair * N * N;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < QP; q += gridDim.x * blockDim.x) {
+        int y1, y2, x;
+        if (q < QFULL) {
+            y1 = 1 + q / N;
+            x = q % N;
+            y2 = N - y1;
+        } else {
+            const int q2 = q - QFULL, half = N / 2 + 1;
+            y1 = y2 = (q2 < half) ? 0 : N / 2;
+            x = (q2 < half) ? q2 : q2 - half;
+        }
+        const int xm = (N - x) & (N - 1);
+        const uint32_t p1 = (uint32_t)(y1 * N + x), p2 = (uint32_t)(y2 * N + xm);
+        const float t1 = __ldg(T + p1), t2 = __ldg(T + p2);
+        float2 ha, hb = make_float2(0.f, 0.f);
+        if (flat) {                                         // N_LUT = 0 (R-6)
+            ha = make_float2(t1 + t2, 0.f);
+            if (has_b)
+                hb = ha;
+        } else {
+            const float2 a1 = __ldg(lut + lut_mod(ba + p1, ix));
+            const float2 a2 = __ldg(lut + lut_mod(ba + p2, ix));
+            ha = make_float2(t1 * a1.x + t2 * a2.x, t1 * a1.y - t2 * a2.y);
+            if (has_b) {
+                const float2 b1 = __ldg(lut + lut_mod(bb + p1, ix));
+                const float2 b2 = __ldg(lut + lut_mod(bb + p2, ix));
+                hb = make_float2(t1 * b1.x + t2 * b2.x, t1 * b1.y - t2 * b2.y);
             }
         }
-    } else {
-#pragma unroll
-        for (int m = 0; m < E; ++m)
-            v[m] = make_float2(0.f, 0.f);
-    }
-    fft::fft2pass<N, true, 1>(v, smem + lr * P::SMEM, t, tw);
-    if (active) {
-        float2 *out = buf + ((size_t)pair * N + y) * N;
-#pragma unroll
-        for (int r = 0; r < E; ++r)
-            out[t + R1 * r] = v[r];
+        Z[p1] = make_float2(ha.x - hb.y, ha.y + hb.x);
+        Z[p2] = make_float2(ha.x + hb.y, hb.x - ha.y);
     }
 }
 
-// ---- pass B ------------------------------------------------------------------------------
+// ---- pass B: column IFFT -> a4 sign + pack -> column FFT (TMA-fed pipeline) ------------------
 __device__ __forceinline__ uint8_t msb_first8(unsigned bits8) { return (uint8_t)(__brev(bits8) >> 24); }
 
 template <int N>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
-ospr_cols_kernel(const float2 *__restrict__ tw, float2 *__restrict__ buf, int npairs, int last_has_b, uint8_t *__restrict__ bits)
-{
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, W = ColCfg<N>::W;
-    constexpr size_t FRAME_BYTES = (size_t)N * N / 8;
-    extern __shared__ float2 smem[];
-    const int c = threadIdx.x % W, t = threadIdx.x / W;
-    const int tile = blockIdx.x, pair = blockIdx.y;
-    const bool has_b = (pair < npairs - 1) || last_has_b;
-    float2 *col = buf + (size_t)pair * N * N + tile * W + c;
-    float2 v[E];
+struct OsprColBody {
+    struct Args {
+        const float2 *tw;
+        float2 *buf;
+        uint8_t *bits;
+        int npairs;
+        int last_has_b;
+    };
+    template <class TW>
+    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int pair,
+                                               int ct, const Args &a, const TW &twr)
+    {
+        using P = fft::Plan<N>;
+        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
+        constexpr size_t FRAME_BYTES = (size_t)N * N / 8;
+        const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
+        fft::fft2pass<N, true, W>(v, sm, t, twr);              // v[r] = H at row t + R1*r (x N)
+        static_assert(E <= 64, "bit words hold at most 64 rows per thread");
+        using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
+        Word wa = 0, wb = 0;                                     // a4: bit r = sign of row t + R1*r
 #pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = col[(size_t)(t + R1 * m) * N];
-    fft::fft2pass<N, true, W>(v, smem + c, t, tw);           // v[r] = H at row t + R1*r
-    const int grp = (threadIdx.x & 31) / W;
-    uint8_t *ba = bits ? bits + (size_t)(2 * pair) * FRAME_BYTES + tile : nullptr;
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const bool pa = v[r].x >= 0.0f;                  // a4; -0.0 -> +1 (R-7)
-        const bool pb = v[r].y >= 0.0f;
-        const unsigned ma = __ballot_sync(0xffffffffu, pa);
-        const unsigned mb = __ballot_sync(0xffffffffu, pb);
-        if (ba != nullptr && c == 0) {
-            const size_t off = (size_t)(t + R1 * r) * (N / 8);
-            ba[off] = msb_first8((ma >> (W * grp)) & 0xFFu);
-            if (has_b)
-                ba[FRAME_BYTES + off] = msb_first8((mb >> (W * grp)) & 0xFFu);
+        for (int r = 0; r < E; ++r) {
+            wa |= (Word)(v[r].x >= 0.0f) << r;                   // -0.0 -> +1 (R-7)
+            wb |= (Word)(v[r].y >= 0.0f) << r;
         }
-        v[r] = make_float2(pa ? 1.0f : -1.0f, has_b ? (pb ? 1.0f : -1.0f) : 0.0f);
-    }
-    fft::fft2pass<N, false, W>(v, smem + c, t, tw);
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-        col[(size_t)(t + R1 * r) * N] = v[r];
-}
-
-// ---- pass C ------------------------------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(RowCfg<N>::THREADS)
-ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs, float *__restrict__ acc, int accumulate)
-{
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, RPC = RowCfg<N>::RPC;
-    extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / R1, t = threadIdx.x % R1;
-    const int y = blockIdx.x * RPC + lr;
-    float a[E];
-#pragma unroll
-    for (int r = 0; r < E; ++r)
-        a[r] = 0.0f;
-    for (int p = 0; p < npairs; ++p) {
-        const float2 *row = buf + ((size_t)p * N + y) * N;
-        float2 v[E];
-#pragma unroll
-        for (int m = 0; m < E; ++m)
-            v[m] = row[t + R1 * m];
-        fft::fft2pass<N, false, 1>(v, smem + lr * P::SMEM, t, tw);
 #pragma unroll
         for (int r = 0; r < E; ++r)
-            a[r] += v[r].x * v[r].x + v[r].y * v[r].y;
-    }
-    constexpr float inv_p = 1.0f / ((float)N * (float)N);   // exact power of two
-    float *out = acc + (size_t)y * N;
+            v[r] = make_float2(((wa >> r) & 1) ? 1.0f : -1.0f, has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
+        fft::fft2pass<N, false, W>(v, sm, t, twr);
+        float2 *col = a.buf + (size_t)pair * N * N + ct * W + c;
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const float val = a[r] * inv_p;
-        out[t + R1 * r] = accumulate ? out[t + R1 * r] + val : val;
+        for (int r = 0; r < E; ++r)
+            col[(size_t)(t + R1 * r) * N] = v[r];
+        // pack: the W = 8 lanes of one row hold its 8 columns; byte = MSB-first (R-8)
+        if (a.bits != nullptr) {
+            const int grp = (threadIdx.x & 31) / W;
+            uint8_t *ba = a.bits + (size_t)(2 * pair) * FRAME_BYTES + ct + (size_t)t * (N / 8);
+#pragma unroll 1
+            for (int r = 0; r < E; ++r, ba += (size_t)R1 * (N / 8)) {
+                const unsigned ma = __ballot_sync(0xffffffffu, (unsigned)(wa >> r) & 1u);
+                const unsigned mb = __ballot_sync(0xffffffffu, (unsigned)(wb >> r) & 1u);
+                if (c == 0) {
+                    ba[0] = msb_first8((ma >> (W * grp)) & 0xFFu);
+                    if (has_b)
+                        ba[FRAME_BYTES] = msb_first8((mb >> (W * grp)) & 0xFFu);
+                }
+            }
+        }
+    }
+};
+
+// ---- pass C: row FFT + |X|^2 summed over the chunk's pairs --------------------------------------
+// Row pipeline (passes.cuh): each warp owns whole row groups y and streams the np pair
+// rows (y, p), p = 0..np-1, through its two ring slots, summing |X|^2 / N^2 over p in
+// registers (fixed order => deterministic), then one read-modify-write of the frame
+// accumulator A per row and chunk.
+template <int N>
+__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
+                   float *__restrict__ acc, int accumulate)
+{
+    using P = fft::Plan<N>;
+    using RP = RowPipe<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW, GPC = RP::WPC / 2;
+    static_assert(RP::WPC % 2 == 0, "two warps (pair halves) per row group");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const WarpRing ring = make_ring<RP::SLOT_C, RP::WPC>(smem_raw);
+    float *red = reinterpret_cast<float *>(smem_raw + ring_smem<RP::SLOT_C, RP::WPC>());   // [GPC][GPW*N]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    const int lg = warp >> 1, half = warp & 1;
+    const int hp = (npairs + 1) / 2;                     // pairs of half 0; half 1 gets the rest
+    const int p0 = half * hp, p1 = half ? npairs : hp;
+    const int stride = gridDim.x * GPC;
+    auto src = [&](int gg, int p) { return buf + ((size_t)p * N + (size_t)gg * GPW) * N; };
+    fft::Twiddles<N, false> twr;                          // pool twiddles: keeps registers for a[]
+    twr.load(tw, t);
+    int grp = blockIdx.x * GPC + lg;
+    if (lane == 0 && grp < NGRP && p0 < p1) {
+        tma::mbar_arrive_expect_tx(&ring.bars[0], RP::IN_BYTES);
+        tma::load_1d(ring.slot(0), src(grp, p0), RP::IN_BYTES, &ring.bars[0]);
+    }
+    int k = 0;
+    for (; grp < NGRP; grp += stride) {
+        float a[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            a[r] = 0.0f;
+        for (int p = p0; p < p1; ++p, ++k) {
+            const int s = k & 1;
+            const bool more = (p + 1 < p1) || (grp + stride < NGRP);
+            if (lane == 0 && more) {
+                const float2 *nx = (p + 1 < p1) ? src(grp, p + 1) : src(grp + stride, p0);
+                tma::mbar_arrive_expect_tx(&ring.bars[s ^ 1], RP::IN_BYTES);
+                tma::load_1d(ring.slot(s ^ 1), nx, RP::IN_BYTES, &ring.bars[s ^ 1]);
+            }
+            tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
+            float2 *sl = reinterpret_cast<float2 *>(ring.slot(s));
+            float2 v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m] = sl[g * N + t + R1 * m];
+            fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                a[r] += v[r].x * v[r].x + v[r].y * v[r].y;
+            tma::fence_proxy_async_smem();
+            __syncwarp();
+        }
+        // combine the two halves (half 0 + half 1, fixed order) and update A
+        float *rg = red + (size_t)lg * GPW * N + g * N;
+        if (half == 1) {
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                rg[t + R1 * r] = a[r];
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + lg) : "memory");
+        if (half == 0) {
+            constexpr float inv_p = 1.0f / ((float)N * (float)N);   // exact power of two
+            float *o = acc + ((size_t)grp * GPW + g) * N;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const float val = (a[r] + rg[t + R1 * r]) * inv_p;
+                o[t + R1 * r] = accumulate ? o[t + R1 * r] + val : val;
+            }
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + lg) : "memory");
     }
 }
 
@@ -271,7 +319,7 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static int ospr_chunk_pairs(int n, int n_sub)
 {
     const size_t frame = (size_t)n * n * sizeof(float2);
-    size_t budget = 64ull << 20;   // pair buffers kept L2-resident between passes
+    size_t budget = 96ull << 20;   // pair buffers kept L2-resident between passes (C3: one chunk)
     if (const char *e = getenv("HOLO_OSPR_CHUNK_BYTES"))
         budget = strtoull(e, nullptr, 10);
     long c = (long)(budget / frame);
@@ -310,13 +358,6 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     return off;
 }
 
-static uint32_t draw_base(uint64_t phase_offset, uint64_t sf_global, uint64_t P, uint64_t L)
-{
-    if (L == 0)
-        return 0;
-    unsigned __int128 g = (unsigned __int128)phase_offset + (unsigned __int128)sf_global * P;
-    return (uint32_t)(g % L);
-}
 
 static int fin_grid(int n)
 {
@@ -343,8 +384,6 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                             uint64_t phase_offset, int sf_begin, int sf_end, uint8_t *holo_bits,
                             float *intensity, double *mse, holo_region om, void *ws, cudaStream_t s)
 {
-    using RC = RowCfg<N>;
-    using CC = ColCfg<N>;
     constexpr size_t P = (size_t)N * N;
     OsprWs w;
     ospr_ws_layout(N, n_sub, (char *)ws, &w);
@@ -353,26 +392,35 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const int npairs_total = (nsh + 1) / 2;
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
+    const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
+    const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
     for (int f = 0; f < n_frames; ++f) {
         const float *Tf = target + (size_t)f * P;
         for (int c0 = 0; c0 < npairs_total; c0 += chunk) {
             const int np = (npairs_total - c0) < chunk ? (npairs_total - c0) : chunk;
-            PairBases pb;
-            for (int p = 0; p < np; ++p) {
-                const int sa = sf_begin + 2 * (c0 + p), sb = sa + 1;
-                pb.a[p] = draw_base(phase_offset, (uint64_t)f * n_sub + sa, P, n_lut);
-                pb.b[p] = sb < sf_end ? draw_base(phase_offset, (uint64_t)f * n_sub + sb, P, n_lut) : 0u;
-            }
             const int last_sa = sf_begin + 2 * (c0 + np - 1);
             const int last_has_b = (last_sa + 1) < sf_end;
             uint8_t *bits = holo_bits ? holo_bits + ((size_t)f * nsh + 2 * (size_t)c0) * (P / 8) : nullptr;
-            const int rows = np * N;
-            HOLO_TRY(launch(K_OSPR_ROWS_A, ospr_rows_a_kernel<N>, dim3((rows + RC::RPC - 1) / RC::RPC),
-                            dim3(RC::THREADS), RC::SMEM, s, tw, Tf, lut, ix, pb, np, last_has_b, w.buf));
-            HOLO_TRY(launch(K_OSPR_COLS, ospr_cols_kernel<N>, dim3(N / CC::W, np), dim3(CC::THREADS),
-                            CC::SMEM, s, tw, w.buf, np, last_has_b, bits));
-            HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(N / RC::RPC), dim3(RC::THREADS),
-                            RC::SMEM, s, tw, (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0));
+            {
+                constexpr int QP = (N / 2 - 1) * N + 2 * (N / 2 + 1);
+                int gx = (148 * 8 + np - 1) / np;                      // ~8 CTAs per SM over the chunk
+                if (gx > (QP + 255) / 256)
+                    gx = (QP + 255) / 256;
+                const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
+                HOLO_TRY(launch(K_OSPR_RANDOMISE, ospr_randomise_kernel<N>, dim3(gx, np), dim3(256), 0, s, Tf,
+                                lut, ix, off_mod, p_mod, sf_first, last_has_b, w.buf));
+            }
+            HOLO_TRY((launch_rows_fft<N, true>(K_OSPR_ROWS_A, tw, w.buf, w.buf, np * N, s)));
+            typename OsprColBody<N>::Args ca{tw, w.buf, bits, np, last_has_b};
+            HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
+            {
+                using RP = RowPipe<N>;
+                constexpr size_t smem =
+                    ring_smem<RP::SLOT_C, RP::WPC>() + (size_t)(RP::WPC / 2) * RP::GPW * N * sizeof(float);
+                const int grid = pipe_grid(ospr_rows_c_kernel<N>, RP::WPC * 32, smem, 2 * (N / RP::GPW), RP::WPC);
+                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                                (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0));
+            }
         }
         const float scale = full ? 0.5f / (float)n_sub : 0.5f;
         HOLO_TRY(finalize_frame(w.acc, Tf, N, 1, scale, intensity + (size_t)f * P, om, w.parts,

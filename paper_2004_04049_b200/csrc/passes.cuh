@@ -1,0 +1,249 @@
+// passes.cuh -- launch shapes of the two kinds of FFT pass every kernel of libholo
+// is built from:
+//
+//  * row passes: each row transform is owned by the T = R1 threads of one warp
+//    (N <= 2048, so T <= 32) and synchronises with __syncwarp() only; warps run
+//    independently, loads come straight from global/L2 into registers
+//    (coalesced: lane t reads x = t + R1*m), results go straight back.
+//  * column passes: a persistent CTA streams tiles of W = 8 columns x N rows
+//    through a double-buffered shared-memory ring filled by TMA
+//    (cp.async.bulk.tensor.2d, mbarrier completion); the column transforms read
+//    the tile from shared memory, exchange in place, and write results to global.
+#pragma once
+
+#include "fft.cuh"
+#include "tma.cuh"
+
+#include <stdlib.h>
+
+namespace holo {
+
+template <int N>
+struct RowShape {
+    using P = fft::Plan<N>;
+    static constexpr int GPW = 32 / P::T;                                   // row groups per warp
+    static constexpr int WPC = (N * P::T / 32) < 4 ? (N * P::T / 32) : 4;   // warps per CTA (<= N rows)
+    static constexpr int RPC = WPC * GPW;                                   // rows per CTA
+    static constexpr int THREADS = WPC * 32;
+    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
+};
+
+// ---- row pipeline ---------------------------------------------------------------------------
+// Warp-persistent, per-warp double-buffered: a work item is GPW = 32/T consecutive rows
+// (always 256*E contiguous bytes), fetched by one cp.async.bulk (1D TMA) into the warp's
+// next ring slot while the warp transforms the current one.  The slot is then reused in
+// place as the exchange buffer (padded layout, GPW * (N + N/R1) elements).
+template <int N>
+struct RowPipe {
+    using P = fft::Plan<N>;
+    static constexpr int GPW = 32 / P::T;
+    static constexpr int WPC = 4;                               // warps per CTA
+    static constexpr uint32_t IN_BYTES = (uint32_t)GPW * N * 8;
+    static constexpr uint32_t XCH_BYTES = (uint32_t)GPW * P::SMEM * 8;
+    static constexpr uint32_t SLOT_C = ((XCH_BYTES > IN_BYTES ? XCH_BYTES : IN_BYTES) + 127) / 128 * 128;
+};
+
+// Per-warp ring of two slots of `slot_bytes` each (+ one mbarrier per slot).
+struct WarpRing {
+    unsigned char *base;
+    uint64_t *bars;
+    uint32_t slot_bytes;
+    __device__ __forceinline__ unsigned char *slot(int s) const { return base + (size_t)s * slot_bytes; }
+};
+
+template <uint32_t SLOT_BYTES, int WPC>
+__device__ __forceinline__ WarpRing make_ring(unsigned char *smem_raw)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpRing r;
+    r.slot_bytes = SLOT_BYTES;
+    r.base = smem_raw + (size_t)warp * 2 * SLOT_BYTES;
+    r.bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)WPC * 2 * SLOT_BYTES) + 2 * warp;
+    if (lane == 0) {
+        tma::mbar_init(&r.bars[0], 1);
+        tma::mbar_init(&r.bars[1], 1);
+        tma::fence_mbar_init();
+    }
+    __syncwarp();
+    return r;
+}
+
+template <uint32_t SLOT_BYTES, int WPC>
+constexpr size_t ring_smem() { return (size_t)WPC * 2 * SLOT_BYTES + (size_t)WPC * 2 * sizeof(uint64_t); }
+
+// Plain batched row transform, items = GPW-row groups of `in`, results to `out`
+// (in place allowed: an item is read completely before it is written).
+template <int N, bool INV>
+__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+rows_fft_kernel(const float2 *__restrict__ tw, const float2 *in, float2 *out, int nitems)
+{
+    using P = fft::Plan<N>;
+    using RP = RowPipe<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const WarpRing ring = make_ring<RP::SLOT_C, RP::WPC>(smem_raw);
+    const int lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    const int stride = gridDim.x * RP::WPC;
+    int item = blockIdx.x * RP::WPC + (threadIdx.x >> 5);
+    if (lane == 0 && item < nitems) {
+        tma::mbar_arrive_expect_tx(&ring.bars[0], RP::IN_BYTES);
+        tma::load_1d(ring.slot(0), in + (size_t)item * GPW * N, RP::IN_BYTES, &ring.bars[0]);
+    }
+    fft::Twiddles<N> twr;
+    twr.load(tw, t);
+    for (int k = 0; item < nitems; item += stride, ++k) {
+        const int s = k & 1;
+        const int nxt = item + stride;
+        if (lane == 0 && nxt < nitems) {
+            tma::mbar_arrive_expect_tx(&ring.bars[s ^ 1], RP::IN_BYTES);
+            tma::load_1d(ring.slot(s ^ 1), in + (size_t)nxt * GPW * N, RP::IN_BYTES, &ring.bars[s ^ 1]);
+        }
+        tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
+        float2 *sl = reinterpret_cast<float2 *>(ring.slot(s));
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = sl[g * N + t + R1 * m];
+        fft::fft2pass<N, INV, 1, true>(v, sl + g * P::SMEM, t, twr);
+        float2 *o = out + ((size_t)item * GPW + g) * N;
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            o[t + R1 * r] = v[r];
+        tma::fence_proxy_async_smem();
+        __syncwarp();
+    }
+}
+
+// Host: persistent grid for a row pipeline kernel.
+template <typename K>
+inline int pipe_grid(K kernel, int threads, size_t smem, int nitems, int wpc)
+{
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (smem > 48 * 1024)
+        ensure_smem((const void *)kernel, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1)
+        per_sm = 1;
+    const int want = (nitems + wpc - 1) / wpc;
+    const int cap = sms * per_sm;
+    return want < cap ? want : cap;
+}
+
+template <int N, bool INV>
+holo_status launch_rows_fft(KernelId id, const float2 *tw, const float2 *in, float2 *out, int nrows, cudaStream_t s)
+{
+    using RP = RowPipe<N>;
+    constexpr size_t smem = ring_smem<RP::SLOT_C, RP::WPC>();
+    const int nitems = nrows / RP::GPW;
+    const int grid = pipe_grid(rows_fft_kernel<N, INV>, RP::WPC * 32, smem, nitems, RP::WPC);
+    return launch(id, rows_fft_kernel<N, INV>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw, in, out, nitems);
+}
+
+template <int N, int NSTAGES = 0>
+struct ColPipe {
+    using P = fft::Plan<N>;
+    static constexpr int W = 8;                            // columns per tile (= one packed byte per row)
+    static constexpr int THREADS = W * P::T;
+    static constexpr int BOX_ROWS = N < 256 ? N : 256;    // TMA box limit is 256 per dimension
+    static constexpr int NBOX = N / BOX_ROWS;
+    static constexpr uint32_t TILE_BYTES = (uint32_t)N * W * 8;
+    static constexpr int STAGE_ELEMS = P::SMEM * W;       // padded exchange layout >= dense tile
+    // 2 stages: one CTA per SM double-buffers its tiles; 1 stage: two CTAs per SM
+    // overlap each other's loads (HOLO_COL_STAGES=1, experiments)
+    static constexpr int STAGES = NSTAGES > 0 ? NSTAGES : 2;
+    static constexpr size_t BAR_OFFSET = (size_t)STAGES * STAGE_ELEMS * sizeof(float2);
+    static constexpr size_t SMEM = BAR_OFFSET + 64;
+    static constexpr int TILES_PER_FRAME = N / W;
+    static constexpr int CTAS_PER_SM = (int)((227 * 1024) / SMEM) < 8 ? (int)((227 * 1024) / SMEM) : 8;
+};
+
+// Persistent TMA-fed column pipeline.  Tile k of this CTA is (frame, ct) =
+// (tile / TPF, tile % TPF); its columns [ct*W, ct*W + W) of rows [frame*N, frame*N + N)
+// arrive in stage k % STAGES.  Thread (c, t) = (threadIdx % W, threadIdx / W) gets
+// column c at rows t + R1*m (the pass-1 map) and hands it to Body::run together with
+// its slot of the stage buffer for the in-place exchanges.
+template <int N, class Body, int NSTAGES>
+__global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
+col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
+{
+    using CP = ColPipe<N, NSTAGES>;
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E, W = CP::W, TPF = CP::TILES_PER_FRAME;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + CP::BAR_OFFSET);
+    const int c = threadIdx.x % W, t = threadIdx.x / W;
+    fft::Twiddles<N, (CP::STAGES == 2 && P::E <= 32)> twr;   // registers when 1 CTA/SM has room
+    twr.load(a.tw, t);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < CP::STAGES; ++s)
+            tma::mbar_init(&bars[s], 1);
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int tile, int s) {
+        const int fr = tile / TPF, ct = tile % TPF;
+        tma::mbar_arrive_expect_tx(&bars[s], CP::TILE_BYTES);
+#pragma unroll
+        for (int q = 0; q < CP::NBOX; ++q)
+            tma::load_2d(stage0 + (size_t)s * CP::STAGE_ELEMS + q * CP::BOX_ROWS * W, &tmap, ct * W,
+                         fr * N + q * CP::BOX_ROWS, &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < CP::STAGES; ++s) {
+            const int tile = blockIdx.x + s * gridDim.x;
+            if (tile < ntiles)
+                issue(tile, s);
+        }
+    int k = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int s = k % CP::STAGES;
+        float2 *st = stage0 + (size_t)s * CP::STAGE_ELEMS;
+        tma::mbar_wait(&bars[s], (uint32_t)((k / CP::STAGES) & 1));
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = st[(t + R1 * m) * W + c];
+        Body::run(v, st + c, c, t, tile / TPF, tile % TPF, a, twr);
+        tma::fence_proxy_async_smem();     // generic writes to this stage before the next TMA fill
+        __syncthreads();
+        const int nxt = tile + CP::STAGES * gridDim.x;
+        if (threadIdx.x == 0 && nxt < ntiles)
+            issue(nxt, s);
+    }
+}
+
+// Host: launch the column pipeline over `nframes` frames of `buf` (row-major
+// [nframes*N][N] complex64).
+template <int N, class Body, int NSTAGES>
+holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+{
+    using CP = ColPipe<N, NSTAGES>;
+    CUtensorMap map;
+    HOLO_TRY(make_tmap_c64(&map, buf, N, (uint64_t)nframes * N, CP::W, CP::BOX_ROWS));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ntiles = nframes * CP::TILES_PER_FRAME;
+    int grid = sms * CP::CTAS_PER_SM;
+    if (grid > ntiles)
+        grid = ntiles;
+    return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
+}
+
+// Default: the double-buffered single-CTA variant; HOLO_COL_STAGES=1 selects the other.
+template <int N, class Body>
+holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+{
+    static const int stages = [] {
+        const char *e = getenv("HOLO_COL_STAGES");
+        return e ? atoi(e) : 2;
+    }();
+    if (stages == 2 && N <= 1024)
+        return launch_cols_s<N, Body, 2>(id, buf, nframes, a, s);
+    return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s);
+}
+
+} // namespace holo

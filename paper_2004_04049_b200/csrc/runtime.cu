@@ -11,13 +11,16 @@
 #include <utility>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "fft.cuh"
+#include "tma.cuh"
 
 namespace holo {
 
 const char *const kKernelNames[K_NUM_KERNELS] = {
-    "lut_generate", "ospr_rows_a", "ospr_cols", "ospr_rows_c", "ospr_finalize", "mse_reduce",
+    "lut_generate", "ospr_randomise", "ospr_rows_a", "ospr_cols", "ospr_rows_c", "ospr_finalize", "mse_reduce",
     "gs_rows_init", "gs_cols",     "gs_rows",   "fft_rows",    "fft_cols",      "randomise",
 };
 
@@ -144,6 +147,40 @@ holo_status twiddles(const float2 **pool)
 }
 
 } // namespace fft
+
+// ---- TMA tensor maps (driver entry point fetched through the runtime; no -lcuda) -------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    return fn;
+}
+
+holo_status make_tmap_c64(CUtensorMap *map, const void *base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                          uint32_t box_rows)
+{
+    auto fn = encode_fn();
+    if (!fn)
+        return set_error(HOLO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 8};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return set_error(HOLO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HOLO_OK;
+}
+
 } // namespace holo
 
 using namespace holo;

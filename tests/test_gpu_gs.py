@@ -122,8 +122,12 @@ def test_gs_flat_and_deterministic():
 
 def test_gs_c4_full_size_sampled():
     """BASELINE configs[3] at full size (1024^2, batch 64, 50 iterations, LUT 2^16,
-    continuous) in the bench's launch configuration: frames 0, 31 and 63 against the
-    oracle along the whole trajectory; every frame by energy and error reduction."""
+    continuous) in the bench's launch configuration.  Every frame: energy and error
+    reduction.  Frames 0 and 63: the fused trajectory equals a chain of gs_step calls
+    bit for bit, and at sampled iterations the oracle's step from the GPU's own R_{k-1}
+    matches (one-step protocol, reading R-22: fp32 rounding perturbs the
+    50-iteration trajectory at the 1e-4 level); the whole trajectory is also compared
+    with the oracle's (1e-4 for the first 10 iterations, 1e-3 sanity after)."""
     w = WORKLOADS["C4"]
     Ts = np.stack([target_for(w, b) for b in range(w.frames)])
     lg, lo = lut_pair(LUT_SEED, 1 << 16)
@@ -132,7 +136,17 @@ def test_gs_c4_full_size_sampled():
     P = w.n * w.n
     assert np.all(np.abs(I.reshape(w.frames, -1).astype(np.float64).sum(1) - P) <= 1e-4 * P)
     assert np.all(E[:, 1:] <= E[:, :-1] * (1 + 1e-5))
-    for b in (0, 31, 63):
-        ref = oracle.gs(Ts[b], w.iters, lo, b * P, 0, (0, w.n, 0, w.n))
-        worst = max(rel(mse[b, k], ref["mse"][k]) for k in range(w.iters))
-        assert worst <= REL_TOL, (b, worst)
+    region = (0, w.n, 0, w.n)
+    for b in (0, 63):
+        tg = cuda_target(Ts[b])
+        r = hb.debug_randomise(tg, lg, b * P).unsqueeze(0)
+        ref = oracle.gs(Ts[b], w.iters, lo, b * P, 0, region)
+        for k in range(w.iters):
+            r_prev = r
+            r, st = hb.gs_step(r, tg, levels=0)
+            assert to_np(st.mse)[0, 0] == mse[b, k], (b, k)         # fused == chain of steps
+            if k + 1 in (1, 2, 5, 10, 25, 50):
+                one = oracle.gs_step(to_np(r_prev[0]).astype(np.complex128), Ts[b], 0, region)
+                assert rel(mse[b, k], one["mse"]) <= REL_TOL, (b, k)
+            tol = REL_TOL if k < 10 else 1e-3
+            assert rel(mse[b, k], ref["mse"][k]) <= tol, (b, k, rel(mse[b, k], ref["mse"][k]))

@@ -180,28 +180,30 @@ def test_ospr_c3_full_parity(L):
 
 @pytest.mark.parametrize("L", [1 << 8, 1 << 12, 1 << 20])
 def test_ospr_c3_sampled_and_degenerate(L):
-    """The other C3 lengths all divide N^2 (pin c3 #13): on the GPU every sub-frame must
-    come out bit-identical; sub-frame 0 is checked against the oracle; MSE of the mean
-    equals the oracle's single-sub-frame MSE."""
+    """The other C3 lengths all divide N^2 (pin c3 #13), so every sub-frame draws the
+    same phases and the oracle's sub-frames are identical: each GPU sub-frame is checked
+    against the oracle's sub-frame 0 (the GPU computes the two sub-frames of a pair as
+    Re and Im of one transform, so they may differ from each other inside the band);
+    the MSE of the mean equals the oracle's single-sub-frame MSE."""
     w = WORKLOADS["C3"]
     T = target_for(w)
     lg, lo = lut_pair(LUT_SEED, L)
     res = hb.ospr_generate(cuda_target(T), w.n_sub, lg)
     bits = to_np(res.bits)[0]
-    assert all(np.array_equal(bits[0], bits[s]) for s in range(w.n_sub))
     _, h_re, I1 = oracle.ospr_subframe(T, lo, 0, want_h=True, want_intensity=True)
-    check_bits(bits[0], h_re, w.n)
-    check_intensity(to_np(res.intensity)[0], oracle.replay_from_bits(bits[:1], w.n))
+    for s in range(w.n_sub):
+        check_bits(bits[s], h_re, w.n)
+    check_intensity(to_np(res.intensity)[0], oracle.replay_from_bits(bits, w.n))
     m_ref = oracle.mse_m1(I1, T, w.omega().as_tuple())
     assert rel(to_np(res.mse)[0], m_ref) <= REL_TOL
 
 
 def test_ospr_c5_sampled():
     """BASELINE configs[4] shape (2048^2, N_SF = 32, L = 2^16), two frames.  L divides
-    N^2 (pin c3 #13), so every sub-frame of a frame must be bit-identical on the GPU;
-    sampled sub-frames (incl. frame 1, cursor f N_SF N^2) are checked against the oracle
-    and each frame's MSE against the oracle's single-sub-frame MSE (equal by the
-    degeneracy)."""
+    N^2 (pin c3 #13), so all oracle sub-frames of a frame are identical: sampled GPU
+    sub-frames of both frames (frame 1 starts at cursor N_SF N^2) are checked against
+    the oracle's, the intensity conditionally on all 32 GPU sub-frames, and each frame's
+    MSE against the oracle's single-sub-frame MSE (equal by the degeneracy)."""
     w = WORKLOADS["C5"]
     Ts = np.stack([target_for(w, f) for f in range(2)])
     lg, lo = lut_pair(LUT_SEED, 1 << 16)
@@ -209,10 +211,8 @@ def test_ospr_c5_sampled():
     bits, I, mse = to_np(res.bits), to_np(res.intensity), to_np(res.mse)
     n, P = w.n, w.n * w.n
     for f in range(2):
-        assert all(np.array_equal(bits[f, 0], bits[f, s]) for s in range(w.n_sub))
-    for f, s in [(0, 0), (0, 31), (1, 0)]:
-        _, h_re, I1 = oracle.ospr_subframe(Ts[f], lo, (f * w.n_sub + s) * P, want_h=True, want_intensity=True)
-        check_bits(bits[f, s], h_re, n)
-        if s == 0:
-            assert rel(mse[f], oracle.mse_m1(I1, Ts[f], w.omega().as_tuple())) <= REL_TOL
-            check_intensity(I[f], oracle.replay_from_bits(bits[f, :1], n))
+        _, h_re, I1 = oracle.ospr_subframe(Ts[f], lo, f * w.n_sub * P, want_h=True, want_intensity=True)
+        for s in (0, 1, 30, 31):
+            check_bits(bits[f, s], h_re, n)
+        assert rel(mse[f], oracle.mse_m1(I1, Ts[f], w.omega().as_tuple())) <= REL_TOL
+        check_intensity(I[f], oracle.replay_from_bits(bits[f], n))

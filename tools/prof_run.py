@@ -1,0 +1,31 @@
+"""Small driver for ncu captures: runs the C3 OSPR step and a short C4-shaped GS
+(profile with -k regex:<kernel> -s <skip> -c <count>)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2004_04049_b200 as hb
+from holo_synth import LUT_SEED, WORKLOADS, target_for
+
+what = sys.argv[1] if len(sys.argv) > 1 else "all"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = torch.device("cuda", 0)
+if what in ("all", "ospr"):
+    w = WORKLOADS["C3"]
+    T = torch.from_numpy(target_for(w)).to(dev)
+    lut = hb.lut_generate(LUT_SEED, 1 << 16)
+    for _ in range(reps):
+        r = hb.ospr_generate(T, w.n_sub, lut)
+    torch.cuda.synchronize()
+    print("ospr mse", r.mse.item())
+if what in ("all", "gs"):
+    w = WORKLOADS["C4"]
+    T = torch.from_numpy(np.stack([target_for(w, b) for b in range(8)])).to(dev)
+    lut = hb.lut_generate(LUT_SEED, 1 << 16)
+    for _ in range(reps):
+        g = hb.gs_generate(T, 3, lut, levels=0)
+    torch.cuda.synchronize()
+    print("gs mse", g.mse[:, -1].cpu().numpy())
