@@ -144,12 +144,6 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def shard(n_units, world, rank):
-    b = (n_units * rank) // world
-    e = (n_units * (rank + 1)) // world
-    return b, e
-
-
 def timed_loop(step_fn, k, w, world, flush):
     """W warm-up steps, then K timed steps, each: flush L2, barrier + sync, events."""
     import torch
@@ -193,7 +187,8 @@ def run_gpu(args):
     w3 = WORKLOADS["C3"]
     n, S, P = w3.n, w3.n_sub, w3.n * w3.n
     T = torch.from_numpy(target_for(w3)).to(dev)
-    sb, se = shard(S, world, rank)
+    from paper_2004_04049_b200.parallel import shard_range
+    sb, se = shard_range(S, world, rank)
     full = (world == 1)
     ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device=dev)
     lut_buf = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
@@ -203,14 +198,17 @@ def run_gpu(args):
     mean_buf = torch.empty((1, n, n), dtype=torch.float32, device=dev)
     mse_buf = torch.empty(1, dtype=torch.float64, device=dev)
 
+    from paper_2004_04049_b200.parallel import ShardedOspr
+    sharded = ShardedOspr(world, rank)
+
     def make_ospr_step(L, lut):
         def step():
-            hb.lut_generate(LUT_SEED, L, out=lut[:L])                       # a0
-            hb.ospr_generate(T, S, lut[:L], sf_range=(sb, se), workspace=ws, out=out)   # a1-a7
-            if not full:
-                import torch.distributed as dist
-                dist.all_reduce(out.intensity)                              # C-1: sum of partial I
-                hb.ospr_finalize(T, out.intensity, S, out=mean_buf)         # a7 after the reduce
+            hb.lut_generate(LUT_SEED, L, out=lut[:L])                               # a0
+            if full:
+                hb.ospr_generate(T, S, lut[:L], workspace=ws, out=out)              # a1-a7
+            else:
+                r = sharded.run(T, S, lut[:L], workspace=ws)                        # a1-a6 shard, C-1, a7
+                out.mse = r.mse
         return step
 
     step = make_ospr_step(args.lut, lut_buf)
@@ -301,15 +299,14 @@ def run_gpu(args):
 
         def e2e_step():
             T_dev.copy_(T_host, non_blocking=True)                              # H2D inputs
-            hb.ospr_generate(T_dev, S, lut_e2e, sf_range=(sb, se), workspace=ws, out=out)
-            if not full:
-                import torch.distributed as dist
-                dist.all_reduce(out.intensity)
-                _, m = hb.ospr_finalize(T_dev, out.intensity, S, out=mean_buf)
-                mse_host.copy_(m, non_blocking=True)
-            else:
+            if full:
+                hb.ospr_generate(T_dev, S, lut_e2e, workspace=ws, out=out)
                 mse_host.copy_(out.mse, non_blocking=True)                      # D2H metric
-            bits_host.copy_(out.bits, non_blocking=True)                        # D2H holograms
+                bits_host.copy_(out.bits, non_blocking=True)                    # D2H holograms
+            else:
+                r = sharded.run(T_dev, S, lut_e2e, workspace=ws)
+                mse_host.copy_(r.mse, non_blocking=True)
+                bits_host.copy_(r.bits, non_blocking=True)
         tm, _ = timed_loop(e2e_step, args.steps, args.warmup, world, flush)
         tm = max_over_ranks(tm, world)
         result["e2e"] = {"value": S * args.steps / (tm / 1e3), "unit": UNIT,
@@ -321,7 +318,8 @@ def run_gpu(args):
     if not args.no_gs:
         w4 = WORKLOADS["C4"]
         B, iters, n4 = w4.frames, w4.iters, w4.n
-        fb, fe = shard(B, world, rank)
+        from paper_2004_04049_b200.parallel import shard_range
+        fb, fe = shard_range(B, world, rank)
         T4 = torch.from_numpy(np.stack([target_for(w4, b) for b in range(fb, fe)])).to(dev)
         lut4 = torch.empty(1 << 16, dtype=torch.complex64, device=dev)
         ws4 = torch.empty(hb.gs_workspace_bytes(n4, fe - fb, iters), dtype=torch.uint8, device=dev)
@@ -330,10 +328,13 @@ def run_gpu(args):
                            mse=torch.empty((fe - fb, iters), dtype=torch.float64, device=dev),
                            err_e=torch.empty((fe - fb, iters), dtype=torch.float64, device=dev))
 
+        from paper_2004_04049_b200.parallel import ShardedGs
+        gsh = ShardedGs(world, rank)
+
         def gs_step():
             hb.lut_generate(LUT_SEED, 1 << 16, out=lut4)
-            hb.gs_generate(T4, iters, lut4, phase_offset=fb * n4 * n4, levels=0, workspace=ws4, out=gout)
-
+            hb.gs_generate(T4, iters, lut4, phase_offset=gsh.frame_range(B)[0] * n4 * n4, levels=0,
+                           workspace=ws4, out=gout)
         ks = args.gs_steps or max(3, args.steps // 4)
         hb.profile_enable(True)
         gm, _ = timed_loop(gs_step, ks, min(args.warmup, 3), world, flush)

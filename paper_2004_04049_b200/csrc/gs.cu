@@ -102,6 +102,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
 // ---- column pass: IFFT -> constraint -> FFT (TMA-fed pipeline) ----------------------------------
 template <int N>
 struct GsColBody {
+    static constexpr int kStages = 1;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *state;

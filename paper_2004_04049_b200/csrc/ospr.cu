@@ -106,6 +106,7 @@ __device__ __forceinline__ uint8_t msb_first8(unsigned bits8) { return (uint8_t)
 
 template <int N>
 struct OsprColBody {
+    static constexpr int kStages = 2;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *buf;

@@ -233,14 +233,15 @@ holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typ
     return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
 }
 
-// Default: the double-buffered single-CTA variant; HOLO_COL_STAGES=1 selects the other.
+// Body::kStages picks the variant (measured per body); HOLO_COL_STAGES overrides it.
 template <int N, class Body>
 holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
 {
-    static const int stages = [] {
+    static const int env_stages = [] {
         const char *e = getenv("HOLO_COL_STAGES");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 0;
     }();
+    const int stages = env_stages ? env_stages : Body::kStages;
     if (stages == 2 && N <= 1024)
         return launch_cols_s<N, Body, 2>(id, buf, nframes, a, s);
     return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s);
