@@ -71,13 +71,26 @@ holo_status launch(KernelId id, void (*kernel)(KArgs...), dim3 grid, dim3 block,
 }
 
 // ---- complex helpers ---------------------------------------------------------------
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// The FFT arithmetic is written with explicit round-to-nearest intrinsics so that the
+// compiler cannot contract it differently in different kernels: every instantiation of a
+// transform performs bit-identical arithmetic (the fused GS loop equals chained gs_step
+// calls, tests/test_gpu_gs.py).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b)
 {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)), __fmaf_rn(a.x, b.y, __fmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// 1/sqrt(x) for x > 0: hardware estimate + one Newton step (about 1 ulp; a few
+// branch-free instructions instead of the IEEE sqrt + divide sequences, whose code
+// size per unrolled element overflows the instruction cache).
+__device__ __forceinline__ float rsqrt_nr(float x)
+{
+    const float r = rsqrtf(x);
+    return __fmul_rn(r, __fmaf_rn(__fmul_rn(-0.5f, x), __fmul_rn(r, r), 1.5f));
+}
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
 // ---- cyclic LUT index (step a1) ----------------------------------------------------------

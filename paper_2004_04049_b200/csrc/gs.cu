@@ -100,64 +100,82 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
 }
 
 // ---- column pass: IFFT -> constraint -> FFT (TMA-fed pipeline) ----------------------------------
-template <int N>
+template <int N, bool QUANT>
 struct GsColBody {
     static constexpr int kStages = 1;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *state;
         int levels;
+        const float2 *qtab;   // Q-entry level table (QUANT only)
         float2 *holo;
         uint8_t *lev;
     };
-    template <class TW>
-    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int fr,
-                                               int tile, const Args &a, const TW &twr)
+    template <class F>
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int fr, int tile,
+                                               const Args &a, const F &fft)
     {
-        using P = fft::Plan<N>;
-        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
+        constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
         const size_t fofs = (size_t)fr * N * N;
-        fft::fft2pass<N, true, W>(v, sm, t, twr);            // H_k (x N)
         const int levels = a.levels;
         const float q_over_2pi = (float)levels * 0.15915494309189533577f;
+        // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            if (h == 0) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-            const float2 h = v[r];
-            float2 o;
-            int j = 0;
-            if (levels == 0) {
-                const float m2 = h.x * h.x + h.y * h.y;
-                if (m2 == 0.0f) {
-                    o = make_float2(1.0f, 0.0f);               // R-16: H = 0 -> +1
-                } else {
-                    const float rr = 1.0f / sqrtf(m2);
-                    o = make_float2(h.x * rr, h.y * rr);
-                }
-            } else {
-                float th = atan2f(h.y, h.x);
-                if (th < 0.0f)
-                    th += 6.28318530717958647692f;
-                j = (int)floorf(th * q_over_2pi + 0.5f);
-                if (j >= levels)
-                    j -= levels;
-                double sn, cs;
-                sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
-                o = make_float2((float)cs, (float)sn);
+                for (int r = 0; r < E; ++r)
+                    v[r].y = -v[r].y;
             }
-            const size_t idx = fofs + (size_t)(t + R1 * r) * N + tile * W + c;
-            if (a.holo != nullptr)
-                a.holo[idx] = o;
-            if (a.lev != nullptr)
-                a.lev[idx] = (uint8_t)j;
-            v[r] = o;
+            fft.template run<false, W>(v, sm, t);
+            if (h == 1)
+                break;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const float2 hk = make_float2(v[r].x, -v[r].y);  // H_k (x N)
+                float2 o;
+                int j = 0;
+                if constexpr (!QUANT) {
+                    const float m2 = hk.x * hk.x + hk.y * hk.y;
+                    if (m2 == 0.0f) {
+                        o = make_float2(1.0f, 0.0f);           // R-16: H = 0 -> +1
+                    } else {
+                        const float rr = rsqrt_nr(m2);
+                        o = make_float2(hk.x * rr, hk.y * rr);
+                    }
+                } else {
+                    float th = atan2f(hk.y, hk.x);
+                    if (th < 0.0f)
+                        th += 6.28318530717958647692f;
+                    j = (int)floorf(th * q_over_2pi + 0.5f);
+                    if (j >= levels)
+                        j -= levels;
+                    o = a.qtab[j];                             // (cos, sin)(2 pi j / Q), built by gs_qtab
+                }
+                const size_t idx = fofs + (size_t)(t + R1 * r) * N + tile * W + c;
+                if (a.holo != nullptr)
+                    a.holo[idx] = o;
+                if (a.lev != nullptr)
+                    a.lev[idx] = (uint8_t)j;
+                v[r] = o;
+            }
         }
-        fft::fft2pass<N, false, W>(v, sm, t, twr);
         float2 *col = a.state + fofs + tile * W + c;
 #pragma unroll
         for (int r = 0; r < E; ++r)
             col[(size_t)(t + R1 * r) * N] = v[r];
     }
 };
+
+// Level table exp(2 pi i j / Q), j < Q, in double then rounded (R-15).
+__global__ void gs_qtab_kernel(int levels, float2 *__restrict__ qtab)
+{
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < levels; j += gridDim.x * blockDim.x) {
+        double sn, cs;
+        sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
+        qtab[j] = make_float2((float)cs, (float)sn);
+    }
+}
 
 // ---- row pass: FFT -> metrics -> amplitude replacement -> IFFT (row pipeline) ---------------------
 enum GsRowMode : int { GS_FUSED = 0, GS_LAST = 1, GS_STEP = 2 };
@@ -186,6 +204,7 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
     fft::Twiddles<N, false> twr;                          // pool twiddles (register budget)
     twr.load(tw, t);
     constexpr float inv_n = 1.0f / (float)N;                 // exact power of two
+    #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int k = 0; item < nitems; item += stride, ++k) {
         const int s = k & 1;
         const int nxt = item + stride;
@@ -196,76 +215,90 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
         const int fr = item / NGRP, grp = item % NGRP;
         const int y = grp * GPW + g;
         const size_t rofs = ((size_t)fr * N + y) * N;
-        float tv[E];
-#pragma unroll
-        for (int r = 0; r < E; ++r)
-            tv[r] = __ldg(T + rofs + t + R1 * r);               // in flight during the FFT
         tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
         float2 *sl = reinterpret_cast<float2 *>(ring.slot(s));
         float2 v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = sl[g * N + t + R1 * m];
-        fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);   // X = N R'_k
         double sums[4] = {0.0, 0.0, 0.0, 0.0};
-        float fe = 0.0f;
+        // forward FFT, then (FUSED) the inverse through the same transform body:
+        // F^-1{x} = conj(F{conj(x)}) exactly (instruction cache: one copy of the FFT code)
+#pragma unroll 1
+        for (int h = 0; h < (MODE == GS_FUSED ? 2 : 1); ++h) {
+            float tv[E];
+            if (h == 0) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-            const int x = t + R1 * r;
-            const float2 X = v[r];
-            const float m2 = X.x * X.x + X.y * X.y;
-            const float I = m2 * (inv_n * inv_n);
-            const float amp = sqrtf(m2) * inv_n;                 // |R'_k|
-            const float tt = tv[r];
-            const float d = amp - tt;
-            fe += d * d;
-            if (in_region(y, x, om)) {
-                const double Id = I, t2 = (double)tt * tt;
-                sums[0] += Id;
-                sums[1] += Id * Id;
-                sums[2] += Id * t2;
+                for (int r = 0; r < E; ++r)
+                    tv[r] = __ldg(T + rofs + t + R1 * r);       // in flight during the FFT
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    v[r].y = -v[r].y;
             }
-            if (MODE == GS_LAST || MODE == GS_STEP) {
-                if (inten != nullptr)
-                    inten[rofs + x] = I;
+            fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);   // h = 0: X = N R'_k
+            if (h == 1) {
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    state[rofs + t + R1 * r] = make_float2(v[r].x, -v[r].y);
+                break;
             }
-            if (MODE != GS_LAST) {
-                float2 R;
-                if (m2 > 0.0f) {
-                    const float sc = tt / sqrtf(m2);
-                    R = make_float2(__fmul_rn(X.x, sc), __fmul_rn(X.y, sc));   // no contraction into the IFFT
-                } else {
-                    R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
+            float fe = 0.0f;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int x = t + R1 * r;
+                const float2 X = v[r];
+                // explicit rounding: identical arithmetic in every instantiation (fused == step)
+                const float m2 = __fmaf_rn(X.x, X.x, __fmul_rn(X.y, X.y));
+                const float I = __fmul_rn(m2, inv_n * inv_n);
+                const float rr = m2 > 0.0f ? rsqrt_nr(m2) : 0.0f;
+                const float amp = __fmul_rn(__fmul_rn(m2, rr), inv_n);   // |R'_k|
+                const float tt = tv[r];
+                const float d = __fsub_rn(amp, tt);
+                fe = __fmaf_rn(d, d, fe);
+                if (in_region(y, x, om)) {
+                    const double Id = I, t2 = __dmul_rn((double)tt, (double)tt);
+                    sums[0] = __dadd_rn(sums[0], Id);
+                    sums[1] = __fma_rn(Id, Id, sums[1]);
+                    sums[2] = __fma_rn(Id, t2, sums[2]);
                 }
-                v[r] = R;
+                if (MODE == GS_LAST || MODE == GS_STEP) {
+                    if (inten != nullptr)
+                        inten[rofs + x] = I;
+                }
+                if (MODE != GS_LAST) {
+                    float2 R;
+                    if (m2 > 0.0f) {
+                        const float sc = __fmul_rn(tt, rr);
+                        R = make_float2(__fmul_rn(X.x, sc), __fmul_rn(X.y, sc));   // no contraction into the IFFT
+                    } else {
+                        R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
+                    }
+                    v[r] = R;
+                }
             }
-        }
-        sums[3] = (double)fe;
-        // warp reduction of the item's sums (lanes of all GPW rows of the item)
+            sums[3] = (double)fe;
+            // warp reduction of the item's sums (lanes of all GPW rows of the item)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            double x = sums[i];
+            for (int i = 0; i < 4; ++i) {
+                double x = sums[i];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                x += __shfl_down_sync(0xffffffffu, x, o);
-            sums[i] = x;
-        }
-        if (lane == 0) {
-            double *dst = parts + (size_t)fr * frame_stride_parts + (size_t)grp * 4;
-            dst[0] = sums[0];
-            dst[1] = sums[1];
-            dst[2] = sums[2];
-            dst[3] = sums[3];
-        }
-        if (MODE == GS_STEP) {
+                for (int o = 16; o > 0; o >>= 1)
+                    x += __shfl_down_sync(0xffffffffu, x, o);
+                sums[i] = x;
+            }
+            if (lane == 0) {
+                double *dst = parts + (size_t)fr * frame_stride_parts + (size_t)grp * 4;
+                dst[0] = sums[0];
+                dst[1] = sums[1];
+                dst[2] = sums[2];
+                dst[3] = sums[3];
+            }
+            if (MODE == GS_STEP) {
 #pragma unroll
-            for (int r = 0; r < E; ++r)
-                r_out[rofs + t + R1 * r] = v[r];
-        } else if (MODE == GS_FUSED) {
-            fft::fft2pass<N, true, 1, true>(v, sl + g * P::SMEM, t, twr);
-#pragma unroll
-            for (int r = 0; r < E; ++r)
-                state[rofs + t + R1 * r] = v[r];
+                for (int r = 0; r < E; ++r)
+                    r_out[rofs + t + R1 * r] = v[r];
+            }
         }
         tma::fence_proxy_async_smem();
         __syncwarp();
@@ -339,6 +372,7 @@ static int gs_nblk(int n)
 }
 
 struct GsWs {
+    float2 *qtab;
     float2 *state;
     double *parts;
     double *tparts;
@@ -349,6 +383,8 @@ static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
     const size_t P = (size_t)n * n;
     const int G = gs_group(n, batch), nblk = gs_nblk(n);
     size_t off = 0;
+    const size_t o_qtab = off;
+    off = al256(off + 65536 * sizeof(float2));
     const size_t o_state = off;
     off = al256(off + (size_t)G * P * sizeof(float2));
     const size_t o_parts = off;
@@ -356,6 +392,7 @@ static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
     const size_t o_tparts = off;
     off = al256(off + (size_t)batch * kGsTBlocks * 2 * sizeof(double));
     if (w) {
+        w->qtab = (float2 *)(base + o_qtab);
         w->state = (float2 *)(base + o_state);
         w->parts = (double *)(base + o_parts);
         w->tparts = (double *)(base + o_tparts);
@@ -384,6 +421,8 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
     const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
     const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
     const size_t pstride = (size_t)iters * RC::NBLK * 4;   // parts per frame
+    if (levels > 0)
+        HOLO_TRY(launch(K_GS_COLS, gs_qtab_kernel, dim3((levels + 255) / 256), dim3(256), 0, s, levels, w.qtab));
     for (int g0 = 0; g0 < batch; g0 += G) {
         const int ng = (batch - g0) < G ? (batch - g0) : G;
         HOLO_TRY(launch(K_GS_ROWS_INIT, gs_prepare_kernel<N>, dim3(kGsTBlocks, ng), dim3(256), 0, s,
@@ -393,9 +432,16 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
         HOLO_TRY((launch_rows_fft<N, true>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));
         for (int k = 0; k < iters; ++k) {
             const bool last = (k == iters - 1);
-            typename GsColBody<N>::Args ca{tw, w.state, levels, (last && holo) ? holo + g0 * P : (float2 *)nullptr,
-                                           (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr};
-            HOLO_TRY((launch_cols<N, GsColBody<N>>(K_GS_COLS, w.state, ng, ca, s)));
+            if (levels == 0) {
+                typename GsColBody<N, false>::Args ca{tw, w.state, 0, nullptr,
+                                                      (last && holo) ? holo + g0 * P : (float2 *)nullptr, nullptr};
+                HOLO_TRY((launch_cols<N, GsColBody<N, false>>(K_GS_COLS, w.state, ng, ca, s)));
+            } else {
+                typename GsColBody<N, true>::Args ca{tw, w.state, levels, w.qtab,
+                                                     (last && holo) ? holo + g0 * P : (float2 *)nullptr,
+                                                     (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr};
+                HOLO_TRY((launch_cols<N, GsColBody<N, true>>(K_GS_COLS, w.state, ng, ca, s)));
+            }
             double *pk = w.parts + (size_t)g0 * pstride + (size_t)k * RC::NBLK * 4;
             const float *Tg = target + g0 * P;
             using RP = RowPipe<N>;

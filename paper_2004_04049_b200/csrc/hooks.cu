@@ -13,13 +13,12 @@ struct HookColBody {
         float2 *buf;
         float scale;
     };
-    template <class TW>
-    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int fr,
-                                               int tile, const Args &a, const TW &twr)
+    template <class F>
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int fr, int tile,
+                                               const Args &a, const F &fft)
     {
-        using P = fft::Plan<N>;
-        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
-        fft::fft2pass<N, INV, W>(v, sm, t, twr);
+        constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
+        fft.template run<INV, W>(v, sm, t);
         float2 *col = a.buf + (size_t)fr * N * N + tile * W + c;
 #pragma unroll
         for (int r = 0; r < E; ++r)

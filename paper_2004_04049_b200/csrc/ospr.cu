@@ -114,27 +114,38 @@ struct OsprColBody {
         int npairs;
         int last_has_b;
     };
-    template <class TW>
-    static __device__ __forceinline__ void run(float2 (&v)[fft::Plan<N>::E], float2 *sm, int c, int t, int pair,
-                                               int ct, const Args &a, const TW &twr)
+    template <class F>
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int pair, int ct,
+                                               const Args &a, const F &fft)
     {
-        using P = fft::Plan<N>;
-        constexpr int R1 = P::R1, E = P::E, W = ColPipe<N>::W;
+        constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
         constexpr size_t FRAME_BYTES = (size_t)N * N / 8;
         const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
-        fft::fft2pass<N, true, W>(v, sm, t, twr);              // v[r] = H at row t + R1*r (x N)
         static_assert(E <= 64, "bit words hold at most 64 rows per thread");
         using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
         Word wa = 0, wb = 0;                                     // a4: bit r = sign of row t + R1*r
+        // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})
+        // exactly, since negation is exact.
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            if (h == 0) {
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-            wa |= (Word)(v[r].x >= 0.0f) << r;                   // -0.0 -> +1 (R-7)
-            wb |= (Word)(v[r].y >= 0.0f) << r;
+                for (int r = 0; r < E; ++r)
+                    v[r].y = -v[r].y;
+            }
+            fft.template run<false, W>(v, sm, t);
+            if (h == 0) {                                        // v = conj(H) (x N): Re H = v.x, Im H = -v.y
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    wa |= (Word)(v[r].x >= 0.0f) << r;           // -0.0 -> +1 (R-7)
+                    wb |= (Word)(v[r].y <= 0.0f) << r;           // Im H = -v.y >= 0
+                }
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    v[r] = make_float2(((wa >> r) & 1) ? 1.0f : -1.0f,
+                                       has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
+            }
         }
-#pragma unroll
-        for (int r = 0; r < E; ++r)
-            v[r] = make_float2(((wa >> r) & 1) ? 1.0f : -1.0f, has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
-        fft::fft2pass<N, false, W>(v, sm, t, twr);
         float2 *col = a.buf + (size_t)pair * N * N + ct * W + c;
 #pragma unroll
         for (int r = 0; r < E; ++r)
@@ -188,11 +199,13 @@ ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf
         tma::load_1d(ring.slot(0), src(grp, p0), RP::IN_BYTES, &ring.bars[0]);
     }
     int k = 0;
+    #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (; grp < NGRP; grp += stride) {
         float a[E];
 #pragma unroll
         for (int r = 0; r < E; ++r)
             a[r] = 0.0f;
+        #pragma unroll 1   // one copy of the transform code (instruction cache)
         for (int p = p0; p < p1; ++p, ++k) {
             const int s = k & 1;
             const bool more = (p + 1 < p1) || (grp + stride < NGRP);

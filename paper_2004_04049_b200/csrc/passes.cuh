@@ -91,6 +91,7 @@ rows_fft_kernel(const float2 *__restrict__ tw, const float2 *in, float2 *out, in
     }
     fft::Twiddles<N> twr;
     twr.load(tw, t);
+    #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int k = 0; item < nitems; item += stride, ++k) {
         const int s = k & 1;
         const int nxt = item + stride;
@@ -104,11 +105,18 @@ rows_fft_kernel(const float2 *__restrict__ tw, const float2 *in, float2 *out, in
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = sl[g * N + t + R1 * m];
-        fft::fft2pass<N, INV, 1, true>(v, sl + g * P::SMEM, t, twr);
+        // the inverse runs the forward body on conjugates: F^-1{x} = conj(F{conj(x)}) exactly,
+        // the same arithmetic as the fused GS row pass (bit-identical gs_step chains)
+        if (INV) {
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m].y = -v[m].y;
+        }
+        fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);
         float2 *o = out + ((size_t)item * GPW + g) * N;
 #pragma unroll
         for (int r = 0; r < E; ++r)
-            o[t + R1 * r] = v[r];
+            o[t + R1 * r] = INV ? make_float2(v[r].x, -v[r].y) : v[r];
         tma::fence_proxy_async_smem();
         __syncwarp();
     }
@@ -141,18 +149,28 @@ holo_status launch_rows_fft(KernelId id, const float2 *tw, const float2 *in, flo
     return launch(id, rows_fft_kernel<N, INV>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw, in, out, nitems);
 }
 
+// ---- column pipeline -------------------------------------------------------------------------
+// FFT policy per size: the two-pass transform.  (The three-pass E = 16 policy
+// fft::ColFft3 doubles the warps per tile but measured slower on B200 at N = 1024:
+// its extra shared-memory exchange outweighs the occupancy gain.)
+template <int N, bool REG>
+struct ColFftFor {
+    using type = fft::ColFft2<N, REG>;
+};
+
 template <int N, int NSTAGES = 0>
 struct ColPipe {
-    using P = fft::Plan<N>;
     static constexpr int W = 8;                            // columns per tile (= one packed byte per row)
-    static constexpr int THREADS = W * P::T;
-    static constexpr int BOX_ROWS = N < 256 ? N : 256;    // TMA box limit is 256 per dimension
-    static constexpr int NBOX = N / BOX_ROWS;
-    static constexpr uint32_t TILE_BYTES = (uint32_t)N * W * 8;
-    static constexpr int STAGE_ELEMS = P::SMEM * W;       // padded exchange layout >= dense tile
     // 2 stages: one CTA per SM double-buffers its tiles; 1 stage: two CTAs per SM
     // overlap each other's loads (HOLO_COL_STAGES=1, experiments)
     static constexpr int STAGES = NSTAGES > 0 ? NSTAGES : 2;
+    using F = typename ColFftFor<N, (STAGES == 2 && fft::Plan<N>::E <= 32)>::type;
+    static constexpr int T = F::T, E = F::E;
+    static constexpr int THREADS = W * T;
+    static constexpr int BOX_ROWS = N < 256 ? N : 256;    // TMA box limit is 256 per dimension
+    static constexpr int NBOX = N / BOX_ROWS;
+    static constexpr uint32_t TILE_BYTES = (uint32_t)N * W * 8;
+    static constexpr int STAGE_ELEMS = F::SMEM * W;       // padded exchange layout >= dense tile
     static constexpr size_t BAR_OFFSET = (size_t)STAGES * STAGE_ELEMS * sizeof(float2);
     static constexpr size_t SMEM = BAR_OFFSET + 64;
     static constexpr int TILES_PER_FRAME = N / W;
@@ -162,21 +180,21 @@ struct ColPipe {
 // Persistent TMA-fed column pipeline.  Tile k of this CTA is (frame, ct) =
 // (tile / TPF, tile % TPF); its columns [ct*W, ct*W + W) of rows [frame*N, frame*N + N)
 // arrive in stage k % STAGES.  Thread (c, t) = (threadIdx % W, threadIdx / W) gets
-// column c at rows t + R1*m (the pass-1 map) and hands it to Body::run together with
-// its slot of the stage buffer for the in-place exchanges.
+// column c at rows t + T*m (the transform's natural map) and hands it to Body::run
+// with its slot of the stage buffer for the in-place exchanges and the FFT policy.
 template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
 {
     using CP = ColPipe<N, NSTAGES>;
-    using P = fft::Plan<N>;
-    constexpr int R1 = P::R1, E = P::E, W = CP::W, TPF = CP::TILES_PER_FRAME;
+    using F = typename CP::F;
+    constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + CP::BAR_OFFSET);
     const int c = threadIdx.x % W, t = threadIdx.x / W;
-    fft::Twiddles<N, (CP::STAGES == 2 && P::E <= 32)> twr;   // registers when 1 CTA/SM has room
-    twr.load(a.tw, t);
+    F fft;
+    fft.init(a.tw, t);
     if (threadIdx.x == 0) {
         for (int s = 0; s < CP::STAGES; ++s)
             tma::mbar_init(&bars[s], 1);
@@ -198,6 +216,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
                 issue(tile, s);
         }
     int k = 0;
+    #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
         const int s = k % CP::STAGES;
         float2 *st = stage0 + (size_t)s * CP::STAGE_ELEMS;
@@ -205,8 +224,8 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
         float2 v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)
-            v[m] = st[(t + R1 * m) * W + c];
-        Body::run(v, st + c, c, t, tile / TPF, tile % TPF, a, twr);
+            v[m] = st[(t + T * m) * W + c];
+        Body::template run<F>(v, st + c, c, t, tile / TPF, tile % TPF, a, fft);
         tma::fence_proxy_async_smem();     // generic writes to this stage before the next TMA fill
         __syncthreads();
         const int nxt = tile + CP::STAGES * gridDim.x;
