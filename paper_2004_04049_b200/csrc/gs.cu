@@ -160,10 +160,7 @@ struct GsColBody {
                 v[r] = o;
             }
         }
-        float2 *col = a.state + fofs + tile * W + c;
-#pragma unroll
-        for (int r = 0; r < E; ++r)
-            col[(size_t)(t + R1 * r) * N] = v[r];
+        // (the pipeline stores v, the column FFT of h_k, with a TMA tile store)
     }
 };
 

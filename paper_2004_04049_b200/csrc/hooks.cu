@@ -19,10 +19,9 @@ struct HookColBody {
     {
         constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
         fft.template run<INV, W>(v, sm, t);
-        float2 *col = a.buf + (size_t)fr * N * N + tile * W + c;
 #pragma unroll
         for (int r = 0; r < E; ++r)
-            col[(size_t)(t + R1 * r) * N] = make_float2(v[r].x * a.scale, v[r].y * a.scale);
+            v[r] = make_float2(v[r].x * a.scale, v[r].y * a.scale);   // stored by the pipeline (TMA)
     }
 };
 

@@ -146,10 +146,7 @@ struct OsprColBody {
                                        has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
             }
         }
-        float2 *col = a.buf + (size_t)pair * N * N + ct * W + c;
-#pragma unroll
-        for (int r = 0; r < E; ++r)
-            col[(size_t)(t + R1 * r) * N] = v[r];
+        // (the pipeline stores v, the column FFT of h', with a TMA tile store)
         // pack: the W = 8 lanes of one row hold its 8 columns; byte = MSB-first (R-8)
         if (a.bits != nullptr) {
             const int grp = (threadIdx.x & 31) / W;

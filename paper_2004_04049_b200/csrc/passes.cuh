@@ -226,12 +226,28 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
         Body::template run<F>(v, st + c, c, t, tile / TPF, tile % TPF, a, fft);
-        tma::fence_proxy_async_smem();     // generic writes to this stage before the next TMA fill
+        // results -> the stage in natural [row][col] layout -> one TMA tile store (in place)
+        __syncthreads();                   // every thread is done with the exchange data
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            st[(t + T * m) * W + c] = v[m];
+        tma::fence_proxy_async_smem();     // generic writes before the async-proxy store/fill
         __syncthreads();
-        const int nxt = tile + CP::STAGES * gridDim.x;
-        if (threadIdx.x == 0 && nxt < ntiles)
-            issue(nxt, s);
+        if (threadIdx.x == 0) {
+            const int fr = tile / TPF, ct = tile % TPF;
+#pragma unroll
+            for (int q = 0; q < CP::NBOX; ++q)
+                tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
+            tma::bulk_commit();
+            const int nxt = tile + CP::STAGES * gridDim.x;
+            if (nxt < ntiles) {
+                tma::bulk_wait_read<0>();  // the store has read the stage; refill it
+                issue(nxt, s);
+            }
+        }
     }
+    if (threadIdx.x == 0)
+        tma::bulk_wait<0>();               // stores complete before the CTA retires
 }
 
 // Host: launch the column pipeline over `nframes` frames of `buf` (row-major

@@ -68,6 +68,30 @@ __device__ __forceinline__ void load_1d(void *dst, const void *src, uint32_t byt
                  : "memory");
 }
 
+// 2D tile store shared -> global (bulk-group completion); the shared tile must not be
+// overwritten before wait_group_read<0>() in the issuing thread.
+__device__ __forceinline__ void store_2d(const CUtensorMap *map, int x, int y, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     (uint64_t)map),
+                 "r"(x), "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N_PENDING>
+__device__ __forceinline__ void bulk_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N_PENDING) : "memory");
+}
+
+template <int N_PENDING>
+__device__ __forceinline__ void bulk_wait()
+{
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N_PENDING) : "memory");
+}
+
 } // namespace tma
 
 // Host: 2D tensor map over a row-major array of 8-byte elements (complex64)
