@@ -30,8 +30,7 @@ holo_status cuda_status(cudaError_t e, const char *where);
 // ---- kernel classes (profiling names) ----------------------------------------------------
 enum KernelId : int {
     K_LUT_GENERATE = 0,
-    K_OSPR_RANDOMISE,   // T x LUT for a sub-frame pair, Hermitian pairing (streaming)
-    K_OSPR_ROWS_A,      // row IFFT
+    K_OSPR_ROWS_A,      // T x LUT for a sub-frame pair (Hermitian pairing) + row IFFT
     K_OSPR_COLS,        // column IFFT + sign quantise + bit pack + column FFT
     K_OSPR_ROWS_C,      // row FFT + |.|^2 accumulate over the chunk's pairs
     K_OSPR_FINALIZE,    // symmetrise/scale + MSE partial sums
@@ -71,15 +70,66 @@ holo_status launch(KernelId id, void (*kernel)(KArgs...), dim3 grid, dim3 block,
 }
 
 // ---- complex helpers ---------------------------------------------------------------
-// The FFT arithmetic is written with explicit round-to-nearest intrinsics so that the
-// compiler cannot contract it differently in different kernels: every instantiation of a
-// transform performs bit-identical arithmetic (the fused GS loop equals chained gs_step
-// calls, tests/test_gpu_gs.py).
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+// Complex arithmetic on sm_100's packed fp32 pipe: one complex add is one
+// add.rn.f32x2 (SASS FADD2), one complex multiply one mul.rn.f32x2 + one
+// fma.rn.f32x2 (FMUL2 + FFMA2), the swaps, broadcasts and sign flips folding into
+// operand modifiers.  Each lane is an IEEE round-to-nearest fp32 operation, and the
+// explicit PTX leaves the compiler nothing to contract, so every instantiation of a
+// transform performs bit-identical arithmetic (the fused GS loop equals chained
+// gs_step calls, tests/test_gpu_gs.py).
+namespace f2 {
+__device__ __forceinline__ unsigned long long pk(float2 a)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 up(unsigned long long r)
+{
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 add(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return up(r);
+}
+__device__ __forceinline__ float2 sub(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return up(r);
+}
+__device__ __forceinline__ float2 mul(float2 a, float2 b)
+{
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return up(r);
+}
+__device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c)
+{
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+    return up(r);
+}
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+} // namespace f2
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2::add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return f2::sub(a, b); }
+// i*a = (-a.y, a.x)
+__device__ __forceinline__ float2 cmul_i(float2 a) { return make_float2(-a.y, a.x); }
+// a*b = (a.x b.x - a.y b.y, a.x b.y + a.y b.x): t = a*b.x (rounded), then fma(i*a, b.y, t)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b)
 {
-    return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)), __fmaf_rn(a.x, b.y, __fmul_rn(a.y, b.x)));
+    return f2::fma(cmul_i(a), f2::bc(b.y), f2::mul(a, f2::bc(b.x)));
+}
+// a * (c + i s) for compile-time c, s (immediate operands)
+__device__ __forceinline__ float2 cmul_cs(float2 a, float c, float s)
+{
+    return f2::fma(cmul_i(a), f2::bc(s), f2::mul(a, f2::bc(c)));
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
@@ -96,40 +146,56 @@ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2
 // ---- cyclic LUT index (step a1) ----------------------------------------------------------
 // idx = (rowbase + x) mod L for rowbase < L, x < N, evaluated per pixel without a
 // hardware divide: L >= N needs at most one subtraction; a power-of-two L is a mask;
-// otherwise Lemire's fastmod (exact for 32-bit operands).
+// otherwise Lemire's fastmod (exact for 32-bit operands).  An empty pool (N_LUT = 0,
+// R-6) is indexed as the one-entry pool {1 + 0i} (L = 1, mask 0).
+enum LutMode : int { LUT_WRAP = 0, LUT_POW2 = 1, LUT_GENERAL = 2 };
 struct LutIndexer {
     uint32_t L;       // N_LUT (> 0)
-    uint32_t mode;    // 0: L >= N (single wrap); 1: power of two; 2: general
-    uint64_t M;       // ceil(2^64 / L) for mode 2
+    uint32_t mode;    // LutMode
+    uint64_t M;       // ceil(2^64 / L) for LUT_GENERAL
     __host__ static LutIndexer make(uint32_t L, uint32_t n)
     {
         LutIndexer r;
         r.L = L;
         r.M = (L & (L - 1)) ? UINT64_MAX / L + 1 : 0;   // Lemire constant (non-powers of two)
         if (L >= n)
-            r.mode = 0;
+            r.mode = LUT_WRAP;
         else if ((L & (L - 1)) == 0)
-            r.mode = 1;
+            r.mode = LUT_POW2;
         else
-            r.mode = 2;
+            r.mode = LUT_GENERAL;
         return r;
+    }
+    // compile-time mode: branch-free per-pixel index
+    template <int MODE>
+    __device__ __forceinline__ uint32_t mod_t(uint32_t a) const
+    {
+        if constexpr (MODE == LUT_WRAP)
+            return a >= L ? a - L : a;
+        else if constexpr (MODE == LUT_POW2)
+            return a & (L - 1);
+        else
+            return (uint32_t)__umul64hi(M * (uint64_t)a, (uint64_t)L);
     }
     __device__ __forceinline__ uint32_t mod(uint32_t a) const
     {
-        if (mode == 0)
-            return a >= L ? a - L : a;
-        if (mode == 1)
-            return a & (L - 1);
-        return (uint32_t)__umul64hi(M * (uint64_t)a, (uint64_t)L);
+        if (mode == LUT_WRAP)
+            return mod_t<LUT_WRAP>(a);
+        if (mode == LUT_POW2)
+            return mod_t<LUT_POW2>(a);
+        return mod_t<LUT_GENERAL>(a);
     }
     // general a (may exceed 2L): used once per row
     __device__ __forceinline__ uint32_t mod_any(uint64_t a) const { return (uint32_t)(a % L); }
 };
 
-// Phase factor for pool entry idx (flat 1+0i when the pool is empty, R-6).
+// Phase factor for pool entry idx.
 __device__ __forceinline__ float2 lut_at(const float2 *__restrict__ lut, uint32_t idx)
 {
     return __ldg(lut + idx);
 }
+
+// The one-entry pool {1 + 0i} standing for N_LUT = 0 (flat phase, R-6).
+static __device__ const float2 k_flat_lut[1] = {{1.0f, 0.0f}};
 
 } // namespace holo

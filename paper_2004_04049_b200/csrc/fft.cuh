@@ -89,20 +89,21 @@ __device__ __forceinline__ float2 tw_mul(float2 x)
         return INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
     } else if constexpr (4 * k == 3 * R) {      // fwd +i, inv -i
         return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
-    } else if constexpr ((8 * k) % R == 0) {    // odd multiples of pi/4
+    } else if constexpr ((8 * k) % R == 0) {    // odd multiples of pi/4: (+-1 +-i)/sqrt2
         constexpr CS w = cs2pi(INV ? k : -k, R);
-        constexpr float sc = w.c > 0 ? 1.0f : -1.0f;
-        constexpr float ss = w.s > 0 ? 1.0f : -1.0f;
         constexpr float h = 0.70710678118654752440f;
-        const float re = sc > 0 ? (ss > 0 ? __fsub_rn(x.x, x.y) : __fadd_rn(x.x, x.y))
-                                : (ss > 0 ? -__fadd_rn(x.x, x.y) : __fsub_rn(x.y, x.x));
-        const float im = sc > 0 ? (ss > 0 ? __fadd_rn(x.x, x.y) : __fsub_rn(x.y, x.x))
-                                : (ss > 0 ? __fsub_rn(x.x, x.y) : -__fadd_rn(x.x, x.y));
-        return make_float2(__fmul_rn(re, h), __fmul_rn(im, h));
+        // x + i x = (x.x - x.y, x.y + x.x), x - i x = (x.x + x.y, x.y - x.x): one FADD2 + one FMUL2
+        if constexpr (w.c > 0 && w.s > 0)
+            return f2::mul(cadd(x, cmul_i(x)), f2::bc(h));
+        else if constexpr (w.c > 0)
+            return f2::mul(csub(x, cmul_i(x)), f2::bc(h));
+        else if constexpr (w.s > 0)
+            return f2::mul(csub(x, cmul_i(x)), f2::bc(-h));
+        else
+            return f2::mul(cadd(x, cmul_i(x)), f2::bc(-h));
     } else {
         constexpr CS w = cs2pi(INV ? k : -k, R);
-        constexpr float c = (float)w.c, s = (float)w.s;
-        return make_float2(__fmaf_rn(x.x, c, -__fmul_rn(x.y, s)), __fmaf_rn(x.x, s, __fmul_rn(x.y, c)));
+        return cmul_cs(x, (float)w.c, (float)w.s);
     }
 }
 

@@ -105,14 +105,15 @@ struct GsColBody {
     static constexpr int kStages = 1;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
-        float2 *state;
+        float2 *buf;          // the group's state (updated in place)
         int levels;
         const float2 *qtab;   // Q-entry level table (QUANT only)
         float2 *holo;
         uint8_t *lev;
     };
     template <class F>
-    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int fr, int tile,
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *, int c, int t, int fr,
+                                               int tile,
                                                const Args &a, const F &fft)
     {
         constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m

@@ -14,7 +14,8 @@ struct HookColBody {
         float scale;
     };
     template <class F>
-    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int fr, int tile,
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *, int c, int t, int fr,
+                                               int tile,
                                                const Args &a, const F &fft)
     {
         constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m

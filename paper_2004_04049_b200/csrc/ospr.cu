@@ -2,11 +2,11 @@
 // steps a1-a7 of DESIGN.md §1) as three fused FFT passes per chunk of
 // sub-frame pairs plus a finalize pass per frame.
 //
-//   pass R  ospr_randomise  R_s = T * lut[(base_s + p) mod L] for the two
-//                        sub-frames a, b of a pair at pixels p and -p, Hermitian
-//                        parts packed as Z = 2 Herm(R_a) + 2i Herm(R_b)
-//                        (so F^-1{Z} = 2 (Re H_a + i Re H_b)).
-//   pass A  ospr_rows_a  row IFFT of Z in place.
+//   pass A  ospr_rows_a  R_s = T * lut[(base_s + p) mod L] for the two sub-frames
+//                        a, b of a pair at pixels p and -p, Hermitian parts packed
+//                        as Z = 2 Herm(R_a) + 2i Herm(R_b) (so F^-1{Z} =
+//                        2 (Re H_a + i Re H_b)), built in shared
+//                        memory and row-IFFTed in the same kernel.
 //   pass B  ospr_cols    column IFFT -> H; a4: bit_a = Re H >= 0, bit_b = Im H >= 0,
 //                        packed MSB-first via warp ballots; h' = (+-1) + i(+-1);
 //                        column FFT of h'; write back in place.
@@ -31,19 +31,11 @@ constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => determini
 constexpr int kFinThreads = 256;
 
 
-// ---- pass R: randomisation (a1, a2) with Hermitian pairing --------------------------------------
-// Streaming kernel, one thread per unordered pixel pair {(y1, x), (y2, xm)} = {p, -p}
-// of one sub-frame pair (a, b).  T and the LUT are read once per pixel:
+// ---- randomisation (a1, a2) with Hermitian pairing ---------------------------------------------
+// For an unordered pixel pair {p, -p} of one sub-frame pair (a, b), T and the LUT are read once:
 //   Ha = R_a(p) + conj(R_a(-p)) = 2 Herm(R_a)(p),   Hb likewise,   R_s = T * lut[(base_s + p) mod L]
 //   Z(p) = Ha + i Hb,   Z(-p) = conj(Ha) + i conj(Hb)   (the Hermitian parts are conjugate-symmetric)
-// so that F^-1{Z} = 2 (Re H_a + i Re H_b) after pass A.  The pair
-// index space is rows y1 in [1, N/2) x all x, plus x in [0, N/2] of rows 0 and N/2.
-__device__ __forceinline__ uint32_t lut_mod(uint32_t a, const LutIndexer &ix)
-{
-    // any 32-bit a; L a power of two (incl. 1) -> mask, else Lemire's exact fastmod
-    return (ix.L & (ix.L - 1)) == 0 ? (a & (ix.L - 1)) : (uint32_t)__umul64hi(ix.M * (uint64_t)a, (uint64_t)ix.L);
-}
-
+// so that F^-1{Z} = 2 (Re H_a + i Re H_b) after pass A.
 // Draw base of global sub-frame s: (off + s * N^2) mod L with off, N^2 reduced mod L on the
 // host (all operands < 2^31, so the 64-bit product cannot overflow).
 __device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, uint32_t p_mod, uint32_t L)
@@ -51,58 +43,133 @@ __device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, 
     return (uint32_t)(((uint64_t)off_mod + (s % L) * (uint64_t)p_mod) % L);
 }
 
-template <int N>
-__global__ void __launch_bounds__(256)
-ospr_randomise_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, LutIndexer ix, uint32_t off_mod,
-                      uint32_t p_mod, uint64_t sf_first, int last_pair_has_b, float2 *__restrict__ buf)
+// Z at the pixel pair {p1, p2 = -p1} of one sub-frame pair (a, b) from T (t1, t2) and the
+// phase factors a1, a2 (sub-frame a) and b1, b2 (sub-frame b) at p1, p2.
+struct ZPair {
+    float2 z1, z2;
+};
+__device__ __forceinline__ ZPair z_pair(float t1, float t2, float2 a1, float2 a2, float2 b1, float2 b2)
 {
-    constexpr int QFULL = (N / 2 - 1) * N;                // pixel pairs in rows 1 .. N/2-1
-    constexpr int QP = QFULL + 2 * (N / 2 + 1);            // per sub-frame pair
-    const int pair = blockIdx.y;
-    const bool has_b = (pair < (int)gridDim.y - 1) || last_pair_has_b;
-    const bool flat = (lut == nullptr);
-    uint32_t ba = 0, bb = 0;
-    if (!flat) {
-        ba = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair, p_mod, ix.L);
-        bb = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair + 1, p_mod, ix.L);
-    }
-    float2 *Z = buf + (size_t)pair * N * N;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < QP; q += gridDim.x * blockDim.x) {
-        int y1, y2, x;
-        if (q < QFULL) {
-            y1 = 1 + q / N;
-            x = q % N;
-            y2 = N - y1;
-        } else {
-            const int q2 = q - QFULL, half = N / 2 + 1;
-            y1 = y2 = (q2 < half) ? 0 : N / 2;
-            x = (q2 < half) ? q2 : q2 - half;
-        }
-        const int xm = (N - x) & (N - 1);
-        const uint32_t p1 = (uint32_t)(y1 * N + x), p2 = (uint32_t)(y2 * N + xm);
-        const float t1 = __ldg(T + p1), t2 = __ldg(T + p2);
-        float2 ha, hb = make_float2(0.f, 0.f);
-        if (flat) {                                         // N_LUT = 0 (R-6)
-            ha = make_float2(t1 + t2, 0.f);
-            if (has_b)
-                hb = ha;
-        } else {
-            const float2 a1 = __ldg(lut + lut_mod(ba + p1, ix));
-            const float2 a2 = __ldg(lut + lut_mod(ba + p2, ix));
-            ha = make_float2(t1 * a1.x + t2 * a2.x, t1 * a1.y - t2 * a2.y);
-            if (has_b) {
-                const float2 b1 = __ldg(lut + lut_mod(bb + p1, ix));
-                const float2 b2 = __ldg(lut + lut_mod(bb + p2, ix));
-                hb = make_float2(t1 * b1.x + t2 * b2.x, t1 * b1.y - t2 * b2.y);
+    const float2 ha = make_float2(t1 * a1.x + t2 * a2.x, t1 * a1.y - t2 * a2.y);
+    const float2 hb = make_float2(t1 * b1.x + t2 * b2.x, t1 * b1.y - t2 * b2.y);
+    return ZPair{make_float2(ha.x - hb.y, ha.y + hb.x), make_float2(ha.x + hb.y, hb.x - ha.y)};
+}
+
+// LUT index base of row y of a sub-frame whose draws start at base: (base + y N) mod L.
+__device__ __forceinline__ uint32_t row_base(uint32_t base, int y, int n, uint32_t L)
+{
+    return (uint32_t)(((uint64_t)base + (uint64_t)y * (uint64_t)n) % L);
+}
+
+// ---- pass A: randomisation (a1, a2) with Hermitian pairing, fused into the row IFFT --------------
+// A warp unit is ROWS rows of one sub-frame pair made of ROWS/2 mirrored row pairs
+// {y, -y mod N}: item 0 = rows {0, N/2} (each its own mirror), item k > 0 = rows {k, N-k}.
+// The warp first builds Z for all the unit's rows in its shared-memory slot, reading T
+// and the LUT once per pixel pair {p, -p} (coalesced rows, L1/L2-resident), then
+// row-IFFTs them GPW rows per round and writes the result (no Z round trip through HBM).
+template <int N>
+struct RowA {
+    using P = fft::Plan<N>;
+    static constexpr int GPW = 32 / P::T;                        // rows per FFT round
+    static constexpr int ROWS = GPW < 2 ? 2 : GPW;               // rows per unit
+    static constexpr int ROUNDS = ROWS / GPW;
+    static constexpr int IPU = ROWS / 2;                         // mirrored row pairs per unit
+    static constexpr int UNITS_PER_PAIR = (N / 2) / IPU;
+    static constexpr int WPC = 4;
+    static constexpr uint32_t SLOT = ((uint32_t)ROWS * P::SMEM * 8 + 127) / 128 * 128;
+    static constexpr size_t SMEM = (size_t)WPC * SLOT;
+};
+
+template <int N, int LMODE>
+__global__ void __launch_bounds__(RowA<N>::WPC * 32)
+ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut_in,
+                   LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t sf_first, int npairs,
+                   int last_pair_has_b, float2 *__restrict__ buf)
+{
+    using P = fft::Plan<N>;
+    using RA = RowA<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RA::GPW, IPU = RA::IPU;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RA::SLOT);
+    const float2 *__restrict__ lut = lut_in != nullptr ? lut_in : k_flat_lut;   // N_LUT = 0: {1 + 0i}, L = 1
+    fft::Twiddles<N> twr;
+    twr.load(tw, t);
+    const int nunits = npairs * RA::UNITS_PER_PAIR;
+    #pragma unroll 1
+    for (int u = blockIdx.x * RA::WPC + warp; u < nunits; u += gridDim.x * RA::WPC) {
+        const int pair = u / RA::UNITS_PER_PAIR, k0 = (u % RA::UNITS_PER_PAIR) * IPU;
+        const bool has_b = (pair < npairs - 1) || last_pair_has_b;
+        const uint32_t ba = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair, p_mod, ix.L);
+        const uint32_t bb = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair + 1, p_mod, ix.L);
+        const float bsc = has_b ? 1.0f : 0.0f;   // an absent sub-frame b contributes R_b = 0
+        // build Z: row slot 2i holds row y, slot 2i+1 its mirror row ym (padded stride P::SMEM).
+        // Rows 0 and N/2 are their own mirrors: their pairs are x <-> N - x, x in [0, N/2].
+#pragma unroll 1
+        for (int j = 0; j < 2 * IPU; j += 2) {
+            const int k = k0 + j / 2;
+            const int y = k > 0 ? k : 0, ym = k > 0 ? N - k : N / 2;
+            float2 *s0 = sl + (size_t)j * P::SMEM, *s1 = s0 + P::SMEM;
+#pragma unroll 1
+            for (int h = 0; h < (k > 0 ? 1 : 2); ++h) {
+                // k > 0: pixel pairs (y, x) <-> (ym, N - x), x < N;  k = 0: (yy, x) <-> (yy, N - x), x <= N/2
+                const int r1 = (k > 0 || h == 0) ? y : ym, r2 = k > 0 ? ym : r1;
+                float2 *d1 = (k > 0 || h == 0) ? s0 : s1, *d2 = k > 0 ? s1 : d1;
+                const int xend = k > 0 ? N : N / 2 + 1;
+                const uint32_t a1 = row_base(ba, r1, N, ix.L), a2 = row_base(ba, r2, N, ix.L);
+                const uint32_t b1 = row_base(bb, r1, N, ix.L), b2 = row_base(bb, r2, N, ix.L);
+                const float *T1 = T + (size_t)r1 * N, *T2 = T + (size_t)r2 * N;
+#pragma unroll 4
+                for (int x = lane; x < xend; x += 32) {
+                    const int xm = (N - x) & (N - 1);
+                    const float t1 = __ldg(T1 + x), t2 = __ldg(T2 + xm);
+                    const float2 la1 = __ldg(lut + ix.template mod_t<LMODE>(a1 + x));
+                    const float2 la2 = __ldg(lut + ix.template mod_t<LMODE>(a2 + xm));
+                    const float2 lb1 = __ldg(lut + ix.template mod_t<LMODE>(b1 + x));
+                    const float2 lb2 = __ldg(lut + ix.template mod_t<LMODE>(b2 + xm));
+                    const ZPair z = z_pair(t1, t2, la1, la2, make_float2(lb1.x * bsc, lb1.y * bsc),
+                                           make_float2(lb2.x * bsc, lb2.y * bsc));
+                    d1[x] = z.z1;
+                    d2[xm] = z.z2;
+                }
             }
         }
-        Z[p1] = make_float2(ha.x - hb.y, ha.y + hb.x);
-        Z[p2] = make_float2(ha.x + hb.y, hb.x - ha.y);
+        __syncwarp();
+        // row IFFT, GPW rows per round: F^-1{x} = conj(F{conj(x)}) (one transform body)
+#pragma unroll 1
+        for (int r = 0; r < RA::ROUNDS; ++r) {
+            const int slot = r * GPW + g;
+            float2 *sg = sl + (size_t)slot * P::SMEM;
+            float2 v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                v[m] = sg[t + R1 * m];
+                v[m].y = -v[m].y;
+            }
+            fft::fft2pass<N, false, 1, true>(v, sg, t, twr);
+            const int k = k0 + slot / 2;
+            const int y = (slot & 1) ? (k > 0 ? N - k : N / 2) : k;
+            float2 *o = buf + ((size_t)pair * N + y) * N;
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                o[t + R1 * m] = make_float2(v[m].x, -v[m].y);
+        }
+        __syncwarp();
     }
 }
 
 // ---- pass B: column IFFT -> a4 sign + pack -> column FFT (TMA-fed pipeline) ------------------
-__device__ __forceinline__ uint8_t msb_first8(unsigned bits8) { return (uint8_t)(__brev(bits8) >> 24); }
+// 8x8 bit-matrix transpose (bit 8i + j <-> bit 8j + i), three masked swap stages.
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
+{
+    uint64_t t;
+    t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    return x ^ t ^ (t << 28);
+}
 
 template <int N>
 struct OsprColBody {
@@ -115,14 +182,16 @@ struct OsprColBody {
         int last_has_b;
     };
     template <class F>
-    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, int c, int t, int pair, int ct,
-                                               const Args &a, const F &fft)
+    static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *scratch, int c, int t,
+                                               int pair, int ct, const Args &a, const F &fft)
     {
         constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
         constexpr size_t FRAME_BYTES = (size_t)N * N / 8;
         const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
-        static_assert(E <= 64, "bit words hold at most 64 rows per thread");
+        static_assert(E <= 64 && W == 8, "bit words hold at most 64 rows per thread; one byte per tile row");
         using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
+        static_assert(2 * W * R1 * sizeof(Word) <= ColPipe<N>::SCRATCH_BYTES, "scratch holds both bit planes");
+        Word *sw = reinterpret_cast<Word *>(scratch);            // [frame 2][t R1][c W] sign words
         Word wa = 0, wb = 0;                                     // a4: bit r = sign of row t + R1*r
         // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})
         // exactly, since negation is exact.
@@ -140,6 +209,8 @@ struct OsprColBody {
                     wa |= (Word)(v[r].x >= 0.0f) << r;           // -0.0 -> +1 (R-7)
                     wb |= (Word)(v[r].y <= 0.0f) << r;           // Im H = -v.y >= 0
                 }
+                sw[t * W + c] = wa;                              // read back after the next FFT's barriers
+                sw[(R1 + t) * W + c] = wb;
 #pragma unroll
                 for (int r = 0; r < E; ++r)
                     v[r] = make_float2(((wa >> r) & 1) ? 1.0f : -1.0f,
@@ -147,19 +218,35 @@ struct OsprColBody {
             }
         }
         // (the pipeline stores v, the column FFT of h', with a TMA tile store)
-        // pack: the W = 8 lanes of one row hold its 8 columns; byte = MSB-first (R-8)
+        // pack (R-8, MSB-first): the byte of tile row y = t' + R1*r holds the 8 columns' sign
+        // bits r of words [f][t'][0..7]; a task gathers 8 rows r = 8*rb .. 8*rb+7 of one t' as
+        // an 8x8 bit matrix (byte 7-c = column c) and transposes it into the 8 row bytes.
         if (a.bits != nullptr) {
-            const int grp = (threadIdx.x & 31) / W;
-            uint8_t *ba = a.bits + (size_t)(2 * pair) * FRAME_BYTES + ct + (size_t)t * (N / 8);
+            constexpr int RG = E < 8 ? 1 : E / 8, RPG = E < 8 ? E : 8, TASKS = 2 * R1 * RG;
 #pragma unroll 1
-            for (int r = 0; r < E; ++r, ba += (size_t)R1 * (N / 8)) {
-                const unsigned ma = __ballot_sync(0xffffffffu, (unsigned)(wa >> r) & 1u);
-                const unsigned mb = __ballot_sync(0xffffffffu, (unsigned)(wb >> r) & 1u);
-                if (c == 0) {
-                    ba[0] = msb_first8((ma >> (W * grp)) & 0xFFu);
-                    if (has_b)
-                        ba[FRAME_BYTES] = msb_first8((mb >> (W * grp)) & 0xFFu);
+            for (int task = threadIdx.x; task < TASKS; task += W * R1) {
+                const int f = task / (R1 * RG), rem = task % (R1 * RG), tt = rem % R1, rb = rem / R1;
+                if (f == 1 && !has_b)
+                    continue;
+                Word q[W];                                       // the 8 words, vector loads
+                if constexpr (sizeof(Word) == 4) {
+                    const uint4 *q4 = reinterpret_cast<const uint4 *>(sw + (f * R1 + tt) * W);
+                    const uint4 lo = q4[0], hi = q4[1];
+                    q[0] = lo.x, q[1] = lo.y, q[2] = lo.z, q[3] = lo.w, q[4] = hi.x, q[5] = hi.y, q[6] = hi.z, q[7] = hi.w;
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < W; ++cc)
+                        q[cc] = sw[(f * R1 + tt) * W + cc];
                 }
+                uint64_t m = 0;
+#pragma unroll
+                for (int cc = 0; cc < W; ++cc)
+                    m |= (uint64_t)((q[cc] >> (8 * rb)) & 0xFFu) << (8 * (7 - cc));
+                m = transpose8x8(m);
+                uint8_t *dst = a.bits + (size_t)(2 * pair + f) * FRAME_BYTES + ct + (size_t)(tt + R1 * 8 * rb) * (N / 8);
+#pragma unroll
+                for (int r = 0; r < RPG; ++r)
+                    dst[(size_t)r * R1 * (N / 8)] = (uint8_t)(m >> (8 * r));
             }
         }
     }
@@ -413,15 +500,14 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const int last_has_b = (last_sa + 1) < sf_end;
             uint8_t *bits = holo_bits ? holo_bits + ((size_t)f * nsh + 2 * (size_t)c0) * (P / 8) : nullptr;
             {
-                constexpr int QP = (N / 2 - 1) * N + 2 * (N / 2 + 1);
-                int gx = (148 * 8 + np - 1) / np;                      // ~8 CTAs per SM over the chunk
-                if (gx > (QP + 255) / 256)
-                    gx = (QP + 255) / 256;
+                using RA = RowA<N>;
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                HOLO_TRY(launch(K_OSPR_RANDOMISE, ospr_randomise_kernel<N>, dim3(gx, np), dim3(256), 0, s, Tf,
-                                lut, ix, off_mod, p_mod, sf_first, last_has_b, w.buf));
+                auto kern = ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
+                          : ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2> : ospr_rows_a_kernel<N, LUT_GENERAL>;
+                const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
+                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut, ix,
+                                off_mod, p_mod, sf_first, np, last_has_b, w.buf));
             }
-            HOLO_TRY((launch_rows_fft<N, true>(K_OSPR_ROWS_A, tw, w.buf, w.buf, np * N, s)));
             typename OsprColBody<N>::Args ca{tw, w.buf, bits, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
             {

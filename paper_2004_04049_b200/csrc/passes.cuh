@@ -172,16 +172,20 @@ struct ColPipe {
     static constexpr uint32_t TILE_BYTES = (uint32_t)N * W * 8;
     static constexpr int STAGE_ELEMS = F::SMEM * W;       // padded exchange layout >= dense tile
     static constexpr size_t BAR_OFFSET = (size_t)STAGES * STAGE_ELEMS * sizeof(float2);
-    static constexpr size_t SMEM = BAR_OFFSET + 64;
+    static constexpr size_t SCRATCH_OFFSET = BAR_OFFSET + 64;
+    static constexpr size_t SCRATCH_BYTES = (size_t)2 * W * T * (E > 32 ? 8 : 4);   // 2 words per thread
+    static constexpr size_t SMEM = SCRATCH_OFFSET + SCRATCH_BYTES;
     static constexpr int TILES_PER_FRAME = N / W;
     static constexpr int CTAS_PER_SM = (int)((227 * 1024) / SMEM) < 8 ? (int)((227 * 1024) / SMEM) : 8;
 };
 
-// Persistent TMA-fed column pipeline.  Tile k of this CTA is (frame, ct) =
+// Persistent TMA-fed column pipeline (TMA loads, direct coalesced stores).  Tile k of this CTA is (frame, ct) =
 // (tile / TPF, tile % TPF); its columns [ct*W, ct*W + W) of rows [frame*N, frame*N + N)
 // arrive in stage k % STAGES.  Thread (c, t) = (threadIdx % W, threadIdx / W) gets
 // column c at rows t + T*m (the transform's natural map) and hands it to Body::run
-// with its slot of the stage buffer for the in-place exchanges and the FFT policy.
+// with its slot of the stage buffer for the in-place exchanges, a 2-words-per-thread
+// scratch area (ordered by the transform's barriers) and the FFT policy; the results
+// go back in place to Body::Args::buf (the array the tensor map describes).
 template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
@@ -192,6 +196,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + CP::BAR_OFFSET);
+    uint32_t *scratch = reinterpret_cast<uint32_t *>(smem_raw + CP::SCRATCH_OFFSET);
     const int c = threadIdx.x % W, t = threadIdx.x / W;
     F fft;
     fft.init(a.tw, t);
@@ -225,29 +230,20 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
-        Body::template run<F>(v, st + c, c, t, tile / TPF, tile % TPF, a, fft);
-        // results -> the stage in natural [row][col] layout -> one TMA tile store (in place)
-        __syncthreads();                   // every thread is done with the exchange data
+        Body::template run<F>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
+        // the stage is free once every thread has done its last exchange read: refill it now,
+        // then store the results straight from registers (each warp instruction writes 4 rows
+        // x 64 contiguous bytes, whole sectors) -- no shared-memory round trip for the output
+        tma::fence_proxy_async_smem();     // generic accesses of the stage before the async refill
+        __syncthreads();
+        const int nxt = tile + CP::STAGES * gridDim.x;
+        if (threadIdx.x == 0 && nxt < ntiles)
+            issue(nxt, s);
+        float2 *o = a.buf + ((size_t)(tile / TPF) * N + t) * N + (tile % TPF) * W + c;
 #pragma unroll
         for (int m = 0; m < E; ++m)
-            st[(t + T * m) * W + c] = v[m];
-        tma::fence_proxy_async_smem();     // generic writes before the async-proxy store/fill
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int fr = tile / TPF, ct = tile % TPF;
-#pragma unroll
-            for (int q = 0; q < CP::NBOX; ++q)
-                tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
-            tma::bulk_commit();
-            const int nxt = tile + CP::STAGES * gridDim.x;
-            if (nxt < ntiles) {
-                tma::bulk_wait_read<0>();  // the store has read the stage; refill it
-                issue(nxt, s);
-            }
-        }
+            o[(size_t)T * m * N] = v[m];
     }
-    if (threadIdx.x == 0)
-        tma::bulk_wait<0>();               // stores complete before the CTA retires
 }
 
 // Host: launch the column pipeline over `nframes` frames of `buf` (row-major
@@ -258,13 +254,10 @@ holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typ
     using CP = ColPipe<N, NSTAGES>;
     CUtensorMap map;
     HOLO_TRY(make_tmap_c64(&map, buf, N, (uint64_t)nframes * N, CP::W, CP::BOX_ROWS));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // persistent grid: SMs x resident CTAs per SM (registers and shared memory both count)
+    const int grid = pipe_grid(col_pipe_kernel<N, Body, NSTAGES>, CP::THREADS, CP::SMEM,
+                               nframes * CP::TILES_PER_FRAME, 1);
     const int ntiles = nframes * CP::TILES_PER_FRAME;
-    int grid = sms * CP::CTAS_PER_SM;
-    if (grid > ntiles)
-        grid = ntiles;
     return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
 }
 
