@@ -7,7 +7,7 @@ namespace holo {
 
 template <int N, bool INV>
 struct HookColBody {
-    static constexpr int kStages = 2;   // measured best column-pipeline variant for this body
+    static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *buf;

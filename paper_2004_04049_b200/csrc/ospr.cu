@@ -173,11 +173,11 @@ __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
 
 template <int N>
 struct OsprColBody {
-    static constexpr int kStages = 2;   // measured best column-pipeline variant for this body
+    static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *buf;
-        uint8_t *bits;
+        uint8_t *bits;        // tile-major sign bytes bt[2 * pair + f][ct][y] (nullable)
         int npairs;
         int last_has_b;
     };
@@ -186,7 +186,6 @@ struct OsprColBody {
                                                int pair, int ct, const Args &a, const F &fft)
     {
         constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
-        constexpr size_t FRAME_BYTES = (size_t)N * N / 8;
         const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
         static_assert(E <= 64 && W == 8, "bit words hold at most 64 rows per thread; one byte per tile row");
         using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
@@ -217,10 +216,12 @@ struct OsprColBody {
                                        has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
             }
         }
-        // (the pipeline stores v, the column FFT of h', with a TMA tile store)
+        // (the pipeline stores v, the column FFT of h')
         // pack (R-8, MSB-first): the byte of tile row y = t' + R1*r holds the 8 columns' sign
         // bits r of words [f][t'][0..7]; a task gathers 8 rows r = 8*rb .. 8*rb+7 of one t' as
-        // an 8x8 bit matrix (byte 7-c = column c) and transposes it into the 8 row bytes.
+        // an 8x8 bit matrix (byte 7-c = column c) and transposes it into the 8 row bytes.  The
+        // bytes go to the tile-major staging layout bt[sub-frame][ct][y] (a warp writes 32
+        // consecutive rows = one sector); ospr_bits_transpose_kernel makes them row-major.
         if (a.bits != nullptr) {
             constexpr int RG = E < 8 ? 1 : E / 8, RPG = E < 8 ? E : 8, TASKS = 2 * R1 * RG;
 #pragma unroll 1
@@ -243,14 +244,33 @@ struct OsprColBody {
                 for (int cc = 0; cc < W; ++cc)
                     m |= (uint64_t)((q[cc] >> (8 * rb)) & 0xFFu) << (8 * (7 - cc));
                 m = transpose8x8(m);
-                uint8_t *dst = a.bits + (size_t)(2 * pair + f) * FRAME_BYTES + ct + (size_t)(tt + R1 * 8 * rb) * (N / 8);
+                uint8_t *dst = a.bits + ((size_t)(2 * pair + f) * (N / 8) + ct) * N + tt + R1 * 8 * rb;
 #pragma unroll
                 for (int r = 0; r < RPG; ++r)
-                    dst[(size_t)r * R1 * (N / 8)] = (uint8_t)(m >> (8 * r));
+                    dst[r * R1] = (uint8_t)(m >> (8 * r));
             }
         }
     }
 };
+
+// Tile-major sign bytes bt[q][ct][y] (ct < N/8, y < N) -> row-major packed holograms
+// out[q][y][ct] (R-8).  Block (y-block, q): YB rows of one sub-frame through shared memory,
+// byte-coalesced on both sides.
+template <int N>
+__global__ void __launch_bounds__(256)
+ospr_bits_transpose_kernel(const uint8_t *__restrict__ bt, uint8_t *__restrict__ out)
+{
+    constexpr int C = N / 8, YB = N < 32 ? N : 32;
+    __shared__ uint8_t sm[C][YB + 1];
+    const int q = blockIdx.y, y0 = blockIdx.x * YB;
+    const uint8_t *src = bt + (size_t)q * C * N + y0;
+    for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
+        sm[i / YB][i % YB] = src[(size_t)(i / YB) * N + i % YB];
+    __syncthreads();
+    uint8_t *dst = out + ((size_t)q * N + y0) * C;
+    for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
+        dst[i] = sm[i % C][i / C];
+}
 
 // ---- pass C: row FFT + |X|^2 summed over the chunk's pairs --------------------------------------
 // Row pipeline (passes.cuh): each warp owns whole row groups y and streams the np pair
@@ -435,6 +455,7 @@ struct OsprWs {
     float2 *buf;
     float *acc;
     double *parts;
+    uint8_t *bt;   // tile-major sign bytes of a chunk
 };
 
 static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
@@ -448,10 +469,13 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     off = align256(off + P * sizeof(float));
     const size_t o_parts = off;
     off = align256(off + (size_t)kFinBlocks * 5 * sizeof(double));
+    const size_t o_bt = off;
+    off = align256(off + (size_t)2 * chunk * P / 8);
     if (w) {
         w->buf = (float2 *)(base + o_buf);
         w->acc = (float *)(base + o_acc);
         w->parts = (double *)(base + o_parts);
+        w->bt = (uint8_t *)(base + o_bt);
     }
     return off;
 }
@@ -508,8 +532,13 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                 HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut, ix,
                                 off_mod, p_mod, sf_first, np, last_has_b, w.buf));
             }
-            typename OsprColBody<N>::Args ca{tw, w.buf, bits, np, last_has_b};
+            typename OsprColBody<N>::Args ca{tw, w.buf, bits ? w.bt : nullptr, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
+            if (bits) {
+                constexpr int YB = N < 32 ? N : 32;
+                HOLO_TRY(launch(K_OSPR_BITS, ospr_bits_transpose_kernel<N>, dim3(N / YB, 2 * np - (last_has_b ? 0 : 1)),
+                                dim3(256), 0, s, (const uint8_t *)w.bt, bits));
+            }
             {
                 using RP = RowPipe<N>;
                 constexpr size_t smem =

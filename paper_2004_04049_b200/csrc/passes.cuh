@@ -161,10 +161,11 @@ struct ColFftFor {
 template <int N, int NSTAGES = 0>
 struct ColPipe {
     static constexpr int W = 8;                            // columns per tile (= one packed byte per row)
-    // 2 stages: one CTA per SM double-buffers its tiles; 1 stage: two CTAs per SM
-    // overlap each other's loads (HOLO_COL_STAGES=1, experiments)
-    static constexpr int STAGES = NSTAGES > 0 ? NSTAGES : 2;
-    using F = typename ColFftFor<N, (STAGES == 2 && fft::Plan<N>::E <= 32)>::type;
+    // 3 stages: one CTA per SM, tile k+2 loading while tile k computes and tile k-1's store
+    // drains; 1 stage: two CTAs per SM overlap each other's loads and stores
+    static constexpr int STAGES = NSTAGES > 0 ? NSTAGES : 3;
+    static constexpr int PREFETCH = STAGES > 1 ? STAGES - 1 : 1;   // tiles in flight ahead
+    using F = typename ColFftFor<N, (STAGES >= 2 && fft::Plan<N>::E <= 32)>::type;
     static constexpr int T = F::T, E = F::E;
     static constexpr int THREADS = W * T;
     static constexpr int BOX_ROWS = N < 256 ? N : 256;    // TMA box limit is 256 per dimension
@@ -176,23 +177,23 @@ struct ColPipe {
     static constexpr size_t SCRATCH_BYTES = (size_t)2 * W * T * (E > 32 ? 8 : 4);   // 2 words per thread
     static constexpr size_t SMEM = SCRATCH_OFFSET + SCRATCH_BYTES;
     static constexpr int TILES_PER_FRAME = N / W;
-    static constexpr int CTAS_PER_SM = (int)((227 * 1024) / SMEM) < 8 ? (int)((227 * 1024) / SMEM) : 8;
 };
 
-// Persistent TMA-fed column pipeline (TMA loads, direct coalesced stores).  Tile k of this CTA is (frame, ct) =
+// Persistent TMA-fed column pipeline.  Tile k of this CTA is (frame, ct) =
 // (tile / TPF, tile % TPF); its columns [ct*W, ct*W + W) of rows [frame*N, frame*N + N)
-// arrive in stage k % STAGES.  Thread (c, t) = (threadIdx % W, threadIdx / W) gets
+// arrive in stage k % STAGES by TMA.  Thread (c, t) = (threadIdx % W, threadIdx / W) gets
 // column c at rows t + T*m (the transform's natural map) and hands it to Body::run
 // with its slot of the stage buffer for the in-place exchanges, a 2-words-per-thread
-// scratch area (ordered by the transform's barriers) and the FFT policy; the results
-// go back in place to Body::Args::buf (the array the tensor map describes).
+// scratch area (ordered by the transform's barriers) and the FFT policy.  The results go
+// back through the stage and one TMA tile store (in place); a stage is refilled once
+// its store has been read out, PREFETCH tiles ahead.
 template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
 {
     using CP = ColPipe<N, NSTAGES>;
     using F = typename CP::F;
-    constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME;
+    constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME, S = CP::STAGES, PF = CP::PREFETCH;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + CP::BAR_OFFSET);
@@ -201,7 +202,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
     F fft;
     fft.init(a.tw, t);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < CP::STAGES; ++s)
+        for (int s = 0; s < S; ++s)
             tma::mbar_init(&bars[s], 1);
         tma::fence_mbar_init();
     }
@@ -215,35 +216,44 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
                          fr * N + q * CP::BOX_ROWS, &bars[s]);
     };
     if (threadIdx.x == 0)
-        for (int s = 0; s < CP::STAGES; ++s) {
-            const int tile = blockIdx.x + s * gridDim.x;
+        for (int j = 0; j < PF; ++j) {
+            const int tile = blockIdx.x + j * gridDim.x;
             if (tile < ntiles)
-                issue(tile, s);
+                issue(tile, j % S);
         }
     int k = 0;
     #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-        const int s = k % CP::STAGES;
+        const int s = k % S;
         float2 *st = stage0 + (size_t)s * CP::STAGE_ELEMS;
-        tma::mbar_wait(&bars[s], (uint32_t)((k / CP::STAGES) & 1));
+        tma::mbar_wait(&bars[s], (uint32_t)((k / S) & 1));
         float2 v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
         Body::template run<F>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
-        // the stage is free once every thread has done its last exchange read: refill it now,
-        // then store the results straight from registers (each warp instruction writes 4 rows
-        // x 64 contiguous bytes, whole sectors) -- no shared-memory round trip for the output
-        tma::fence_proxy_async_smem();     // generic accesses of the stage before the async refill
-        __syncthreads();
-        const int nxt = tile + CP::STAGES * gridDim.x;
-        if (threadIdx.x == 0 && nxt < ntiles)
-            issue(nxt, s);
-        float2 *o = a.buf + ((size_t)(tile / TPF) * N + t) * N + (tile % TPF) * W + c;
+        // results -> the stage in natural [row][col] layout -> one TMA tile store (in place)
+        __syncthreads();                   // every thread is done with the exchange data
 #pragma unroll
         for (int m = 0; m < E; ++m)
-            o[(size_t)T * m * N] = v[m];
+            st[(t + T * m) * W + c] = v[m];
+        tma::fence_proxy_async_smem();     // generic writes before the async-proxy store
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int fr = tile / TPF, ct = tile % TPF;
+#pragma unroll
+            for (int q = 0; q < CP::NBOX; ++q)
+                tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
+            tma::bulk_commit();
+            const int nxt = tile + PF * gridDim.x;   // -> stage (k + PF) % S, last stored by tile k + PF - S
+            if (nxt < ntiles) {
+                tma::bulk_wait_read<(S > 1 ? 1 : 0)>();
+                issue(nxt, (k + PF) % S);
+            }
+        }
     }
+    if (threadIdx.x == 0)
+        tma::bulk_wait<0>();               // stores complete before the CTA retires
 }
 
 // Host: launch the column pipeline over `nframes` frames of `buf` (row-major
@@ -261,7 +271,7 @@ holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typ
     return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
 }
 
-// Body::kStages picks the variant (measured per body); HOLO_COL_STAGES overrides it.
+// Body::kStages (3 or 1) picks the variant (measured per body); HOLO_COL_STAGES overrides it.
 template <int N, class Body>
 holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
 {
@@ -270,8 +280,8 @@ holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typen
         return e ? atoi(e) : 0;
     }();
     const int stages = env_stages ? env_stages : Body::kStages;
-    if (stages == 2 && N <= 1024)
-        return launch_cols_s<N, Body, 2>(id, buf, nframes, a, s);
+    if (stages == 3 && N <= 1024)
+        return launch_cols_s<N, Body, 3>(id, buf, nframes, a, s);
     return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s);
 }
 
