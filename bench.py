@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gs-steps", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every step eagerly instead of replaying a captured CUDA graph")
     return ap.parse_args()
 
 
@@ -170,6 +172,71 @@ def timed_loop(step_fn, k, w, world, flush):
     return total, per
 
 
+def graphed(step_fn, enabled):
+    """Capture one step (after it has run eagerly once, so every one-off host set-up --
+    twiddle tables, shared-memory opt-ins -- is done) into a CUDA graph and return its
+    replay; the step's kernels then launch without per-kernel host overhead."""
+    if not enabled:
+        return step_fn
+    import torch
+    step_fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step_fn()
+    torch.cuda.synchronize()
+    return g.replay
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or (None, None)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        e = d["kernels"][kernel]
+        return e["dram_bytes_per_launch"], d["source"]
+    except Exception:
+        return None, None
+
+
+def kernel_times(hb, step_fn, steps, flush, use_graph):
+    """{kernel class: launches, total_ms, avg_us} over `steps` steps.  Graph mode captures the
+    step once more with libholo's profiling on (event-record nodes around every kernel) and
+    reads the events after each replay; eager mode brackets each launch directly."""
+    import torch
+    acc = {}
+
+    def collect():
+        for name in hb.kernel_names():
+            cnt, ms = hb.profile_read(name)
+            if cnt:
+                a = acc.setdefault(name, [0, 0.0])
+                a[0] += cnt
+                a[1] += ms
+
+    hb.profile_enable(True)
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step_fn()
+        torch.cuda.synchronize()
+        for _ in range(steps):
+            flush()
+            g.replay()
+            torch.cuda.synchronize()
+            collect()
+    else:
+        for _ in range(steps):
+            flush()
+            step_fn()
+        torch.cuda.synchronize()
+        collect()
+    hb.profile_enable(False)
+    if use_graph:
+        del g
+    return {k: {"launches": v[0], "total_ms": v[1], "avg_us": 1e3 * v[1] / v[0]} for k, v in acc.items()}
+
+
 def run_gpu(args):
     import torch
     import paper_2004_04049_b200 as hb
@@ -212,41 +279,38 @@ def run_gpu(args):
         return step
 
     step = make_ospr_step(args.lut, lut_buf)
+    use_graph = not args.no_graph and world == 1
     l0 = hb.launch_count()
+    step()
+    launches_per_step = hb.launch_count() - l0                 # libholo kernels in one step
+    timed_step = graphed(step, use_graph)
     with Clocks(local) as clk:
-        total_ms, per = timed_loop(step, args.steps, args.warmup, world, flush)
-    launches = (hb.launch_count() - l0)
-    launches_timed = launches * args.steps // (args.steps + args.warmup)
+        total_ms, per = timed_loop(timed_step, args.steps, args.warmup, world, flush)
+    launches_timed = launches_per_step * args.steps
     total_ms = max_over_ranks(total_ms, world)
     ms_step = total_ms / args.steps
     value = S * args.steps / (total_ms / 1e3)
 
-    # per-kernel device time over a second pass of K steps with event bracketing
-    hb.profile_enable(True)
-    for _ in range(args.steps):
-        flush()
-        step()
-    torch.cuda.synchronize()
-    kern = {}
-    for name in hb.kernel_names():
-        cnt, ms = hb.profile_read(name)
-        if cnt:
-            kern[name] = {"launches": cnt, "total_ms": ms, "avg_us": 1e3 * ms / cnt}
-    hb.profile_enable(False)
+    # per-kernel device time: the same step in the same launch configuration, every kernel
+    # bracketed by CUDA events on its launch stream, K more steps after an L2 flush each
+    kern = kernel_times(hb, step, args.steps, flush, use_graph)
     step_kernel_ms = sum(v["total_ms"] for v in kern.values()) / args.steps
 
     # roofline of the dominant kernel (algorithmic bytes per launch)
-    chunk = max(1, min(16, (64 << 20) // (P * 8), (S + 1) // 2))
     npairs = (se - sb + 1) // 2
+    chunk = hb.ospr_chunk_pairs(n, S)
     nchunks = -(-npairs // chunk)
-    pairs_per_launch = npairs / nchunks
-    bytes_per_pair = {
-        "ospr_rows_a": 4 * P + 8 * P + 2 * 8 * min(args.lut, P),   # T, Z out, LUT entries touched
-        "ospr_cols": 8 * P + 8 * P + P // 4,                        # Z in/out, 2 bit planes
-        "ospr_rows_c": 8 * P,                                       # X in (+ acc RMW per chunk)
+    np_l = npairs / nchunks                                      # pairs per launch (average)
+    nsub_l = (se - sb) / nchunks                                 # sub-frames per launch
+    alg_bytes = {                                                # DESIGN.md §7 table
+        "ospr_rows_a": 4 * P + 8 * min(args.lut, 2 * np_l * P) + 8 * P * np_l,
+        "ospr_cols": 16 * P * np_l + nsub_l * P / 8,
+        "ospr_bits": 2 * nsub_l * P / 8,
+        "ospr_rows_c": 8 * P * np_l + 4 * P + (4 * P if nchunks > 1 else 0) * (nchunks - 1) / nchunks,
+        "ospr_finalize": 12 * P,
     }
-    dom = max((k for k in kern if k in bytes_per_pair), key=lambda k: kern[k]["total_ms"])
-    per_launch = bytes_per_pair[dom] * pairs_per_launch + (8 * P / 1 if dom == "ospr_rows_c" else 0)
+    dom = max((k for k in kern if k in alg_bytes), key=lambda k: kern[k]["total_ms"])
+    per_launch = alg_bytes[dom]
     achieved = per_launch / (kern[dom]["avg_us"] * 1e-6) / 1e9
     peaks = {}
     try:
@@ -255,6 +319,7 @@ def run_gpu(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     share = kern[dom]["total_ms"] / args.steps / step_kernel_ms
+    traffic, traffic_src = ncu_traffic(dom)
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -265,10 +330,11 @@ def run_gpu(args):
                                "a1-a7 incl. MSE); BASELINE configs[2]",
                    "n": n, "n_sub": S, "lut_len": args.lut, "lut_seed": LUT_SEED,
                    "l2": "flushed before every timed step (256 MiB write)",
+                   "launch": "CUDA graph replay of the step (captured once)" if use_graph else "eager launches",
                    "parallelism": f"sub-frame shards x{world}" + (" + NCCL all-reduce of intensity" if world > 1 else "")},
         "gpu_launches": launches_timed,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": kern[dom]["avg_us"],
                      "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "kernels": kern,
@@ -282,7 +348,7 @@ def run_gpu(args):
         sweep = {}
         big = torch.empty(max(w3.lut_lens), dtype=torch.complex64, device=dev)
         for L in w3.lut_lens:
-            st = make_ospr_step(L, big)
+            st = graphed(make_ospr_step(L, big), use_graph)
             tm, _ = timed_loop(st, max(3, args.steps // 2), 2, world, flush)
             sweep[str(L)] = {"sub_frames_per_s": S * max(3, args.steps // 2) / (tm / 1e3),
                              "ms_per_step": tm / max(3, args.steps // 2), "mse": float(out.mse.item())}
@@ -336,17 +402,12 @@ def run_gpu(args):
             hb.gs_generate(T4, iters, lut4, phase_offset=gsh.frame_range(B)[0] * n4 * n4, levels=0,
                            workspace=ws4, out=gout)
         ks = args.gs_steps or max(3, args.steps // 4)
-        hb.profile_enable(True)
-        gm, _ = timed_loop(gs_step, ks, min(args.warmup, 3), world, flush)
-        gk = {}
-        for name in ("gs_rows_init", "gs_cols", "gs_rows", "mse_reduce", "lut_generate"):
-            cnt, ms = hb.profile_read(name)
-            if cnt:
-                gk[name] = {"launches": cnt, "total_ms": ms, "avg_us": 1e3 * ms / cnt}
-        hb.profile_enable(False)
+        gs_timed = graphed(gs_step, use_graph)
+        gm, _ = timed_loop(gs_timed, ks, min(args.warmup, 3), world, flush)
+        gk = kernel_times(hb, gs_step, 1, flush, use_graph)
         gm = max_over_ranks(gm, world)
         P4 = n4 * n4
-        g = min(16, max(1, (32 << 20) // (P4 * 8)), fe - fb)
+        g = hb.gs_group_frames(n4, fe - fb)
         gbytes = {"gs_cols": 16 * P4 * g, "gs_rows": 20 * P4 * g}
         gdom = max(gbytes, key=lambda k: gk.get(k, {"total_ms": 0})["total_ms"])
         gach = gbytes[gdom] / (gk[gdom]["avg_us"] * 1e-6) / 1e9
@@ -354,7 +415,8 @@ def run_gpu(args):
             "metric": "GS 1024^2 iterations/s", "unit": "frame-iterations/s",
             "value": B * iters * ks / (gm / 1e3), "ms_per_step": gm / ks, "steps": ks,
             "config": {"workload": "C4: GS 1024x1024, 64 frames x 50 iterations, continuous phase-only, "
-                                   "LUT 2^16; BASELINE configs[3]", "frames_per_rank": fe - fb},
+                                   "LUT 2^16; BASELINE configs[3]", "frames_per_rank": fe - fb,
+                       "launch": "CUDA graph replay" if use_graph else "eager launches"},
             "roofline": {"bound": "hbm", "kernel": gdom, "achieved": gach, "peak": hbm_peak, "unit": "GB/s",
                          "frac": gach / hbm_peak, "algorithmic_bytes_per_launch": gbytes[gdom],
                          "avg_launch_us": gk[gdom]["avg_us"]},

@@ -128,6 +128,12 @@ holo_status holo_lut_generate(uint64_t seed, uint64_t n_lut, holo_c64 *lut, holo
  * ------------------------------------------------------------------------ */
 size_t holo_ospr_workspace_size(int32_t n, int32_t n_frames, int32_t n_sub);
 
+/* Plan query (instrumentation): the number of sub-frame pairs each chunk of
+ * holo_ospr_generate(n, ..., n_sub, ...) transforms per pass (DESIGN.md §5,
+ * L2-resident pair buffers; HOLO_OSPR_CHUNK_BYTES overrides the 96 MiB budget);
+ * 0 for invalid n or n_sub. */
+int32_t holo_ospr_chunk_pairs(int32_t n, int32_t n_sub);
+
 holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
                                const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset,
                                int32_t sf_begin, int32_t sf_end, uint8_t *holo_bits,
@@ -138,8 +144,11 @@ holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames,
  * cross-rank sum of holo_ospr_generate partial sums): intensity_mean =
  * intensity_sum / n_sub (in place allowed), mse as step a7.
  * intensity_sum, intensity_mean: [n_frames][n][n]; mse: [n_frames] or NULL;
- * ws: only needed if mse != NULL, at least 23680 bytes (592 x 5 doubles;
- * any holo_ospr_workspace_size buffer is large enough). */
+ * ws: only needed if mse != NULL, at least holo_ospr_finalize_workspace_size()
+ * bytes (per-CTA fp64 partial sums and a completion ticket; any
+ * holo_ospr_workspace_size buffer is large enough).  Reductions run in a fixed
+ * order: the result is deterministic. */
+size_t holo_ospr_finalize_workspace_size(void);
 holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, int32_t n,
                                int32_t n_frames, int32_t n_sub, holo_region omega,
                                float *intensity_mean, double *mse, void *ws, size_t ws_bytes,
@@ -171,6 +180,11 @@ holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, 
  *   mse, err_e   [batch][iters] fp64; NULL = skip
  * ------------------------------------------------------------------------ */
 size_t holo_gs_workspace_size(int32_t n, int32_t batch, int32_t iters);
+
+/* Plan query (instrumentation): frames per launch group of holo_gs_generate(n,
+ * batch, ...) (HOLO_GS_GROUP_BYTES overrides the 128 MiB budget);
+ * 0 for invalid n or batch. */
+int32_t holo_gs_group_frames(int32_t n, int32_t batch);
 
 holo_status holo_gs_generate(const float *target, int32_t n, int32_t batch, int32_t iters,
                              const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset,
@@ -213,7 +227,12 @@ uint64_t holo_launch_count(void);
  * bracketed by CUDA events recorded on its launch stream.  holo_profile_read
  * synchronises those events and returns, for the kernel class `name` (e.g.
  * "ospr_cols"), the number of launches and their summed device time in ms
- * since the last enable; returns HOLO_ERR_INVALID_ARG for an unknown name. */
+ * since the last enable; returns HOLO_ERR_INVALID_ARG for an unknown name.
+ * Launches made while the stream is being captured into a CUDA graph are
+ * bracketed by event-record nodes (cudaEventRecordExternal) instead, so after
+ * each replay of that graph holo_profile_read returns the replay's times; the
+ * graph must not outlive the next holo_profile_enable(1), which recycles the
+ * events. */
 holo_status holo_profile_enable(int32_t on);
 holo_status holo_profile_read(const char *name, uint64_t *launches, double *total_ms);
 

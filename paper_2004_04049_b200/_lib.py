@@ -41,6 +41,9 @@ SIGNATURES = {
     "holo_version": (C.c_char_p, []),
     "holo_lut_generate": (C.c_int, [_u64, _u64, _vp, _vp]),
     "holo_ospr_workspace_size": (_sz, [_i32, _i32, _i32]),
+    "holo_ospr_chunk_pairs": (_i32, [_i32, _i32]),
+    "holo_ospr_finalize_workspace_size": (_sz, []),
+    "holo_gs_group_frames": (_i32, [_i32, _i32]),
     "holo_ospr_generate": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _u64, _u64, _i32, _i32, _vp, _vp, _vp,
                                      HoloRegion, _vp, _sz, _vp]),
     "holo_ospr_finalize": (C.c_int, [_vp, _vp, _i32, _i32, _i32, HoloRegion, _vp, _vp, _vp, _sz, _vp]),

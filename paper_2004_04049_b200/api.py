@@ -19,7 +19,7 @@ import torch
 from ._lib import HoloRegion, check, lib
 
 __all__ = [
-    "lut_generate", "ospr_workspace_bytes", "ospr_generate", "ospr_finalize", "gs_workspace_bytes",
+    "lut_generate", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize", "gs_workspace_bytes",
     "gs_generate", "gs_step", "fft2", "debug_randomise", "launch_count", "profile_enable", "profile_read",
     "kernel_names", "version", "default_omega", "OsprResult", "GsResult",
 ]
@@ -88,6 +88,16 @@ def ospr_workspace_bytes(n: int, n_frames: int, n_sub: int) -> int:
     return int(lib().holo_ospr_workspace_size(n, n_frames, n_sub))
 
 
+def ospr_chunk_pairs(n: int, n_sub: int) -> int:
+    """Sub-frame pairs per chunk of the OSPR plan (instrumentation)."""
+    return int(lib().holo_ospr_chunk_pairs(n, n_sub))
+
+
+def gs_group_frames(n: int, batch: int) -> int:
+    """Frames per launch group of the GS plan (instrumentation)."""
+    return int(lib().holo_gs_group_frames(n, batch))
+
+
 def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] = None, phase_offset: int = 0,
                   sf_range: Optional[Tuple[int, int]] = None, want_bits: bool = True, want_mse: bool = True,
                   omega: Optional[Sequence[int]] = None, workspace: Optional[torch.Tensor] = None,
@@ -126,7 +136,7 @@ def ospr_finalize(target: torch.Tensor, intensity_sum: torch.Tensor, n_sub: int,
     om = omega if omega is not None else default_omega(n, "ospr")
     out = torch.empty_like(intensity_sum) if out is None else out
     mse = torch.empty(F, dtype=torch.float64, device=t3.device) if want_mse else None
-    ws = torch.empty(592 * 5 * 8, dtype=torch.uint8, device=t3.device)
+    ws = torch.empty(int(lib().holo_ospr_finalize_workspace_size()), dtype=torch.uint8, device=t3.device)
     check(lib().holo_ospr_finalize(t3.data_ptr(), intensity_sum.data_ptr(), n, F, n_sub, _region(om),
                                    out.data_ptr(), _ptr(mse), ws.data_ptr(), ws.numel(), _stream(t3.device)))
     return out, mse

@@ -52,6 +52,23 @@ void prof_after(KernelId id, cudaStream_t s);
 void count_launch();
 holo_status ensure_smem(const void *fn, size_t smem);
 
+// Programmatic dependent launch (PDL): every library kernel is launched with programmatic
+// stream serialisation and begins with HOLO_PDL_ENTRY: it waits for the previous kernel in
+// the stream to complete and flush (griddepcontrol.wait) before touching memory, and each
+// CTA signals on its way out (any return path) that the next kernel may be scheduled
+// (griddepcontrol.launch_dependents).  The next pass's launch and prologue thus overlap
+// this pass's tail instead of following a full drain; ordering is unchanged.  (Signalling
+// at entry instead measured slower: early dependents' waiting CTAs share the SMs with the
+// running pass.)
+struct PdlExitTrigger {
+    __device__ __forceinline__ ~PdlExitTrigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+};
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define HOLO_PDL_ENTRY()                        \
+    ::holo::PdlExitTrigger holo_pdl_exit_trigger_; \
+    ::holo::pdl_wait()
+bool pdl_enabled();   // HOLO_PDL=0 launches without the attribute (griddepcontrol then no-ops)
+
 template <typename... KArgs, typename... Args>
 holo_status launch(KernelId id, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                    cudaStream_t s, Args... args)
@@ -61,8 +78,19 @@ holo_status launch(KernelId id, void (*kernel)(KArgs...), dim3 grid, dim3 block,
     if (smem > 48 * 1024)
         HOLO_TRY(ensure_smem((const void *)kernel, smem));
     prof_before(id, s);
-    kernel<<<grid, block, smem, s>>>(args...);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    if (e == cudaSuccess)
+        e = cudaGetLastError();
     prof_after(id, s);
     count_launch();
     if (e != cudaSuccess)

@@ -16,7 +16,7 @@
 
 namespace holo {
 
-constexpr int kMaxGroup = 16;
+constexpr int kMaxGroup = 64;
 
 template <int N>
 struct GsRowCfg {
@@ -69,6 +69,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
                   uint32_t p_mod, uint64_t frame0, const float2 *__restrict__ r_in, holo_region om,
                   float2 *__restrict__ state, double *__restrict__ tparts)
 {
+    HOLO_PDL_ENTRY();
     constexpr int P = N * N;
     const int fr = blockIdx.y;
     const float *Tf = T + (size_t)fr * P;
@@ -168,6 +169,7 @@ struct GsColBody {
 // Level table exp(2 pi i j / Q), j < Q, in double then rounded (R-15).
 __global__ void gs_qtab_kernel(int levels, float2 *__restrict__ qtab)
 {
+    HOLO_PDL_ENTRY();
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < levels; j += gridDim.x * blockDim.x) {
         double sn, cs;
         sincospi(2.0 * (double)j / (double)levels, &sn, &cs);
@@ -187,6 +189,7 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                float *__restrict__ inten, float2 *__restrict__ r_out, double *__restrict__ parts,
                size_t frame_stride_parts)
 {
+    HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
     using RP = RowPipe<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW;
@@ -308,6 +311,7 @@ __global__ void __launch_bounds__(128)
 gs_mse_kernel(const double *__restrict__ parts, const double *__restrict__ tparts, int nblk, int iters,
               double inv_count, double *__restrict__ mse, double *__restrict__ err_e)
 {
+    HOLO_PDL_ENTRY();
     const int b = blockIdx.x / iters;
     const double *p = parts + (size_t)blockIdx.x * nblk * 4;
     const double *q = tparts + (size_t)b * kGsTBlocks * 2;
@@ -342,7 +346,7 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 static int gs_group(int n, int batch)
 {
     const size_t frame = (size_t)n * n * sizeof(float2);
-    size_t budget = 32ull << 20;   // state of a group stays L2-resident across iterations
+    size_t budget = 128ull << 20;  // frames per launch group (measured: larger groups amortise pass tails)
     if (const char *e = getenv("HOLO_GS_GROUP_BYTES"))
         budget = strtoull(e, nullptr, 10);
     long g = (long)(budget / frame);
@@ -516,6 +520,13 @@ static holo_status gs_check_common(const float *target, int32_t n, int32_t batch
                    "holo_levels needs 2 <= levels <= 256");
     HOLO_TRY(check_region(om, n));
     return HOLO_OK;
+}
+
+extern "C" int32_t holo_gs_group_frames(int32_t n, int32_t batch)
+{
+    if (check_n(n) != HOLO_OK || batch < 1)
+        return 0;
+    return gs_group(n, batch);
 }
 
 extern "C" holo_status holo_gs_generate(const float *target, int32_t n, int32_t batch, int32_t iters,

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256)
 randomise_kernel(const float *__restrict__ T, int P, const float2 *__restrict__ lut, LutIndexer ix, uint32_t base,
                  float2 *__restrict__ r_out)
 {
+    HOLO_PDL_ENTRY();
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
         const float t = T[p];
         if (lut == nullptr) {

@@ -80,6 +80,7 @@ __device__ __forceinline__ float2 r5_phase(uint32_t u)
 // Grid-stride over entries; 64-bit counter (full-length pools exceed 2^24).
 __global__ void __launch_bounds__(256) lut_generate_kernel(uint64_t seed, uint64_t n_lut, float2 *lut)
 {
+    HOLO_PDL_ENTRY();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_lut; k += stride)
         lut[k] = r5_phase((uint32_t)(splitmix64_at(seed, k) >> 32));

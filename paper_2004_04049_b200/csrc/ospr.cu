@@ -29,6 +29,7 @@ constexpr int kMaxChunk = 64;
 
 constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => deterministic sums)
 constexpr int kFinThreads = 256;
+constexpr size_t kFinWsBytes = (size_t)kFinBlocks * 5 * sizeof(double) + 256;   // partial sums + ticket
 
 
 // ---- randomisation (a1, a2) with Hermitian pairing ---------------------------------------------
@@ -86,6 +87,7 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
                    LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t sf_first, int npairs,
                    int last_pair_has_b, float2 *__restrict__ buf)
 {
+    HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
     using RA = RowA<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RA::GPW, IPU = RA::IPU;
@@ -254,22 +256,51 @@ struct OsprColBody {
 };
 
 // Tile-major sign bytes bt[q][ct][y] (ct < N/8, y < N) -> row-major packed holograms
-// out[q][y][ct] (R-8).  Block (y-block, q): YB rows of one sub-frame through shared memory,
-// byte-coalesced on both sides.
+// out[q][y][ct] (R-8).  Block (y-block, q): YB rows of one sub-frame through shared memory;
+// 32-bit words on both global sides when N >= 32 (every thread's loads in flight at once).
 template <int N>
 __global__ void __launch_bounds__(256)
 ospr_bits_transpose_kernel(const uint8_t *__restrict__ bt, uint8_t *__restrict__ out)
 {
+    HOLO_PDL_ENTRY();
     constexpr int C = N / 8, YB = N < 32 ? N : 32;
-    __shared__ uint8_t sm[C][YB + 1];
+    __shared__ __align__(16) uint8_t sm[C][YB + 4];
     const int q = blockIdx.y, y0 = blockIdx.x * YB;
     const uint8_t *src = bt + (size_t)q * C * N + y0;
-    for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
-        sm[i / YB][i % YB] = src[(size_t)(i / YB) * N + i % YB];
-    __syncthreads();
     uint8_t *dst = out + ((size_t)q * N + y0) * C;
-    for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
-        dst[i] = sm[i % C][i / C];
+    if constexpr (N >= 32) {
+        constexpr int WPR = YB / 4, WORDS = C * WPR, PER = (WORDS + 255) / 256;   // words per ct row
+        uint32_t w[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + 256 * j;
+            w[j] = i < WORDS ? __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(i / WPR) * N) + i % WPR) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + 256 * j;
+            if (i < WORDS)
+                *reinterpret_cast<uint32_t *>(&sm[i / WPR][4 * (i % WPR)]) = w[j];
+        }
+        __syncthreads();
+        constexpr int OW = C / 4;   // output words per row
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + 256 * j;
+            if (i < WORDS) {
+                const int y = i / OW, c4 = 4 * (i % OW);
+                const uint32_t v = (uint32_t)sm[c4][y] | ((uint32_t)sm[c4 + 1][y] << 8) |
+                                   ((uint32_t)sm[c4 + 2][y] << 16) | ((uint32_t)sm[c4 + 3][y] << 24);
+                reinterpret_cast<uint32_t *>(dst + (size_t)y * C)[i % OW] = v;
+            }
+        }
+    } else {
+        for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
+            sm[i / YB][i % YB] = src[(size_t)(i / YB) * N + i % YB];
+        __syncthreads();
+        for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
+            dst[i] = sm[i % C][i / C];
+    }
 }
 
 // ---- pass C: row FFT + |X|^2 summed over the chunk's pairs --------------------------------------
@@ -282,6 +313,7 @@ __global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
 ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
                    float *__restrict__ acc, int accumulate)
 {
+    HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
     using RP = RowPipe<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW, GPC = RP::WPC / 2;
@@ -379,26 +411,41 @@ __device__ __forceinline__ void block_reduce_store(double (&s)[5], int nvals, do
     }
 }
 
-// intensity[k] = (A[k] + A[-k]) * scale (symmetrise = 1) or A[k] * scale; optional
-// fp64 partial sums (sum I, sum I^2, sum I T^2, sum T^2, sum T^4) over Omega.
+// R-12 from the five fp64 sums: a = S_T2 / S_I (0 if S_I = 0);
+// mse = (a^2 S_II - 2 a S_IT2 + S_T4) / |Omega|.
+__device__ __forceinline__ double mse_from_sums(const double *o, double inv_count)
+{
+    const double a = o[0] == 0.0 ? 0.0 : o[3] / o[0];
+    const double sum = a * a * o[1] - 2.0 * a * o[2] + o[4];
+    return (sum > 0.0 ? sum : 0.0) * inv_count;
+}
+
+// intensity[k] = (A[k] + A[-k]) * scale (symmetrise = 1) or A[k] * scale; optional fp64
+// partial sums (sum I, sum I^2, sum I T^2, sum T^2, sum T^4) over Omega, one slot per CTA.
+// With mse != NULL the last CTA to finish (atomic ticket on *counter, which the host zeroes
+// before the launch and the last CTA re-zeroes) reduces the slots in CTA order -- a fixed
+// order, so the MSE is deterministic -- and writes R-12.
 __global__ void __launch_bounds__(kFinThreads)
 ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T, int n, int symmetrise,
-                     float scale, float *out, holo_region om, double *__restrict__ parts)
+                     float scale, float *out, holo_region om, double *__restrict__ parts, unsigned *counter,
+                     double inv_count, double *__restrict__ mse)
 {
+    HOLO_PDL_ENTRY();
     const int P = n * n;
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P; k += gridDim.x * blockDim.x) {
         const int y = k / n, x = k - y * n;
         float I;
         if (symmetrise) {
             const int km = ((n - y) & (n - 1)) * n + ((n - x) & (n - 1));
-            I = (acc[k] + acc[km]) * scale;
+            I = (__ldg(acc + k) + __ldg(acc + km)) * scale;
         } else {
-            I = acc[k] * scale;
+            I = __ldg(acc + k) * scale;
         }
         out[k] = I;
         if (parts != nullptr && y >= om.row0 && y < om.row1 && x >= om.col0 && x < om.col1) {
-            const double Id = I, tt = T[k], t2 = tt * tt;
+            const double Id = I, tt = __ldg(T + k), t2 = tt * tt;
             s[0] += Id;
             s[1] += Id * Id;
             s[2] += Id * t2;
@@ -406,28 +453,31 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
             s[4] += t2 * t2;
         }
     }
-    if (parts != nullptr)
-        block_reduce_store(s, 5, parts + (size_t)blockIdx.x * 5);
-}
-
-// One CTA per frame: fixed-order reduction of nblk x 5 partial sums, then R-12:
-// a = S_T2 / S_I (0 if S_I = 0); mse = (a^2 S_II - 2 a S_IT2 + S_T4) / |Omega|.
-__global__ void __launch_bounds__(256)
-mse_reduce_kernel(const double *__restrict__ parts, int nblk, size_t frame_stride, double inv_count,
-                  double *__restrict__ mse)
-{
-    const double *p = parts + (size_t)blockIdx.x * frame_stride;
-    double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x)
+    if (parts == nullptr)
+        return;
+    block_reduce_store(s, 5, parts + (size_t)blockIdx.x * 5);
+    if (mse == nullptr)
+        return;
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();                                   // this CTA's slot before its ticket
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last)
+        return;
+    __threadfence();
+    double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
         for (int i = 0; i < 5; ++i)
-            s[i] += p[(size_t)b * 5 + i];
-    __shared__ double out[5];
-    block_reduce_store(s, 5, out);
+            t[i] += __ldcg(parts + (size_t)b * 5 + i);
+    __shared__ double o[5];
+    __syncthreads();
+    block_reduce_store(t, 5, o);
     __syncthreads();
     if (threadIdx.x == 0) {
-        const double a = out[0] == 0.0 ? 0.0 : out[3] / out[0];
-        const double sum = a * a * out[1] - 2.0 * a * out[2] + out[4];
-        mse[blockIdx.x] = (sum > 0.0 ? sum : 0.0) * inv_count;
+        *mse = mse_from_sums(o, inv_count);
+        *counter = 0u;
     }
 }
 
@@ -468,7 +518,7 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     const size_t o_acc = off;
     off = align256(off + P * sizeof(float));
     const size_t o_parts = off;
-    off = align256(off + (size_t)kFinBlocks * 5 * sizeof(double));
+    off = align256(off + kFinWsBytes);
     const size_t o_bt = off;
     off = align256(off + (size_t)2 * chunk * P / 8);
     if (w) {
@@ -491,14 +541,15 @@ holo_status finalize_frame(const float *acc, const float *T, int n, int symmetri
                            float *out, holo_region om, double *parts, double *mse, cudaStream_t s)
 {
     const int grid = fin_grid(n);
-    HOLO_TRY(launch(K_OSPR_FINALIZE, ospr_finalize_kernel, dim3(grid), dim3(kFinThreads), 0, s, acc, T,
-                    n, symmetrise, scale, out, om, mse ? parts : (double *)nullptr));
+    unsigned *counter = reinterpret_cast<unsigned *>(parts + (size_t)kFinBlocks * 5);
+    const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
     if (mse) {
-        const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
-        HOLO_TRY(launch(K_MSE_REDUCE, mse_reduce_kernel, dim3(1), dim3(256), 0, s, (const double *)parts,
-                        grid, (size_t)0, 1.0 / cnt, mse));
+        cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+        if (e != cudaSuccess)
+            return cuda_status(e, "cudaMemsetAsync(finalize ticket)");
     }
-    return HOLO_OK;
+    return launch(K_OSPR_FINALIZE, ospr_finalize_kernel, dim3(grid), dim3(kFinThreads), 0, s, acc, T, n, symmetrise,
+                  scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse);
 }
 
 template <int N>
@@ -582,6 +633,15 @@ extern "C" size_t holo_ospr_workspace_size(int32_t n, int32_t n_frames, int32_t 
     return ospr_ws_layout(n, n_sub, nullptr, nullptr);
 }
 
+extern "C" size_t holo_ospr_finalize_workspace_size(void) { return kFinWsBytes; }
+
+extern "C" int32_t holo_ospr_chunk_pairs(int32_t n, int32_t n_sub)
+{
+    if (check_n(n) != HOLO_OK || n_sub < 1)
+        return 0;
+    return ospr_chunk_pairs(n, n_sub);
+}
+
 extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
                                           const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset,
                                           int32_t sf_begin, int32_t sf_end, uint8_t *holo_bits,
@@ -634,7 +694,7 @@ extern "C" holo_status holo_ospr_finalize(const float *target, const float *inte
     HOLO_CHECK_ARG(n_frames >= 1 && n_sub >= 1, "n_frames and n_sub must be >= 1");
     HOLO_CHECK_ARG(target && intensity_sum && intensity_mean, "target, intensity_sum, intensity_mean required");
     HOLO_TRY(check_region(omega, n));
-    const size_t need = (size_t)kFinBlocks * 5 * sizeof(double);
+    const size_t need = kFinWsBytes;
     if (mse) {
         HOLO_CHECK_ARG(ws != nullptr, "workspace is NULL");
         if (ws_bytes < need)

@@ -77,6 +77,7 @@ template <int N, bool INV>
 __global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
 rows_fft_kernel(const float2 *__restrict__ tw, const float2 *in, float2 *out, int nitems)
 {
+    HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
     using RP = RowPipe<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW;
@@ -191,6 +192,7 @@ template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
 {
+    HOLO_PDL_ENTRY();
     using CP = ColPipe<N, NSTAGES>;
     using F = typename CP::F;
     constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME, S = CP::STAGES, PF = CP::PREFETCH;

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <map>
 #include <set>
@@ -66,7 +67,27 @@ static cudaEvent_t take_event()
     return e;
 }
 
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = getenv("HOLO_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Inside a stream capture the events become event-record nodes of the graph
+// (cudaEventRecordExternal), so every replay re-times the captured kernels.
+static void record(cudaEvent_t e, cudaStream_t s)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, s);
+}
 
 void prof_before(KernelId id, cudaStream_t s)
 {
@@ -75,7 +96,7 @@ void prof_before(KernelId id, cudaStream_t s)
         return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     t_pending = take_event();
-    cudaEventRecord(t_pending, s);
+    record(t_pending, s);
 }
 
 void prof_after(KernelId id, cudaStream_t s)
@@ -84,7 +105,7 @@ void prof_after(KernelId id, cudaStream_t s)
         return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = take_event();
-    cudaEventRecord(b, s);
+    record(b, s);
     g_recs.push_back(ProfRec{(int)id, t_pending, b});
     t_pending = nullptr;
 }
