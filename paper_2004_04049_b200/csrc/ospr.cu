@@ -27,6 +27,17 @@ namespace holo {
 
 constexpr int kMaxChunk = 64;
 
+// Device address of this translation unit's one-entry pool {1 + 0i} (common.cuh).
+static holo_status flat_lut(const float2 **p)
+{
+    void *a = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&a, k_flat_lut);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaGetSymbolAddress(k_flat_lut)");
+    *p = (const float2 *)a;
+    return HOLO_OK;
+}
+
 constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => deterministic sums)
 constexpr int kFinThreads = 256;
 constexpr size_t kFinWsBytes = (size_t)kFinBlocks * 5 * sizeof(double) + 256;   // partial sums + ticket
@@ -49,11 +60,14 @@ __device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, 
 struct ZPair {
     float2 z1, z2;
 };
-__device__ __forceinline__ ZPair z_pair(float t1, float t2, float2 a1, float2 a2, float2 b1, float2 b2)
+__device__ __forceinline__ ZPair z_pair(float t1, float t2, float tb1, float tb2, float2 a1, float2 a2, float2 b1,
+                                        float2 b2)
 {
-    const float2 ha = make_float2(t1 * a1.x + t2 * a2.x, t1 * a1.y - t2 * a2.y);
-    const float2 hb = make_float2(t1 * b1.x + t2 * b2.x, t1 * b1.y - t2 * b2.y);
-    return ZPair{make_float2(ha.x - hb.y, ha.y + hb.x), make_float2(ha.x + hb.y, hb.x - ha.y)};
+    // Ha = t1 a1 + t2 conj(a2),  Hb = tb1 b1 + tb2 conj(b2)  (tb = t, or 0 for an absent b)
+    const float2 ha = f2::fma(conjf2(a2), f2::bc(t2), f2::mul(a1, f2::bc(t1)));
+    const float2 hb = f2::fma(conjf2(b2), f2::bc(tb2), f2::mul(b1, f2::bc(tb1)));
+    // Z(p) = Ha + i Hb,  Z(-p) = conj(Ha) + i conj(Hb) = (Ha.x + Hb.y, Hb.x - Ha.y)
+    return ZPair{cadd(ha, cmul_i(hb)), cadd(conjf2(ha), make_float2(hb.y, hb.x))};
 }
 
 // LUT index base of row y of a sub-frame whose draws start at base: (base + y N) mod L.
@@ -83,7 +97,7 @@ struct RowA {
 
 template <int N, int LMODE>
 __global__ void __launch_bounds__(RowA<N>::WPC * 32)
-ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut_in,
+ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut,
                    LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t sf_first, int npairs,
                    int last_pair_has_b, float2 *__restrict__ buf)
 {
@@ -94,7 +108,6 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
     float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RA::SLOT);
-    const float2 *__restrict__ lut = lut_in != nullptr ? lut_in : k_flat_lut;   // N_LUT = 0: {1 + 0i}, L = 1
     fft::Twiddles<N> twr;
     twr.load(tw, t);
     const int nunits = npairs * RA::UNITS_PER_PAIR;
@@ -110,29 +123,46 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
 #pragma unroll 1
         for (int j = 0; j < 2 * IPU; j += 2) {
             const int k = k0 + j / 2;
-            const int y = k > 0 ? k : 0, ym = k > 0 ? N - k : N / 2;
             float2 *s0 = sl + (size_t)j * P::SMEM, *s1 = s0 + P::SMEM;
-#pragma unroll 1
-            for (int h = 0; h < (k > 0 ? 1 : 2); ++h) {
-                // k > 0: pixel pairs (y, x) <-> (ym, N - x), x < N;  k = 0: (yy, x) <-> (yy, N - x), x <= N/2
-                const int r1 = (k > 0 || h == 0) ? y : ym, r2 = k > 0 ? ym : r1;
-                float2 *d1 = (k > 0 || h == 0) ? s0 : s1, *d2 = k > 0 ? s1 : d1;
-                const int xend = k > 0 ? N : N / 2 + 1;
-                const uint32_t a1 = row_base(ba, r1, N, ix.L), a2 = row_base(ba, r2, N, ix.L);
-                const uint32_t b1 = row_base(bb, r1, N, ix.L), b2 = row_base(bb, r2, N, ix.L);
-                const float *T1 = T + (size_t)r1 * N, *T2 = T + (size_t)r2 * N;
-#pragma unroll 4
-                for (int x = lane; x < xend; x += 32) {
+            if (k > 0) {   // pixel pairs (k, x) <-> (N - k, N - x), x < N: N/32 per lane
+                const int y = k, ym = N - k;
+                const uint32_t a1 = row_base(ba, y, N, ix.L), a2 = row_base(ba, ym, N, ix.L);
+                const uint32_t b1 = row_base(bb, y, N, ix.L), b2 = row_base(bb, ym, N, ix.L);
+                const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
+                constexpr int M = N < 32 ? 1 : N / 32;
+#pragma unroll 8
+                for (int m = 0; m < M; ++m) {
+                    const int x = lane + 32 * m;
+                    if (N < 32 && x >= N)
+                        break;
                     const int xm = (N - x) & (N - 1);
-                    const float t1 = __ldg(T1 + x), t2 = __ldg(T2 + xm);
-                    const float2 la1 = __ldg(lut + ix.template mod_t<LMODE>(a1 + x));
-                    const float2 la2 = __ldg(lut + ix.template mod_t<LMODE>(a2 + xm));
-                    const float2 lb1 = __ldg(lut + ix.template mod_t<LMODE>(b1 + x));
-                    const float2 lb2 = __ldg(lut + ix.template mod_t<LMODE>(b2 + xm));
-                    const ZPair z = z_pair(t1, t2, la1, la2, make_float2(lb1.x * bsc, lb1.y * bsc),
-                                           make_float2(lb2.x * bsc, lb2.y * bsc));
-                    d1[x] = z.z1;
-                    d2[xm] = z.z2;
+                    const float t1 = T1[x], t2 = T2[xm];
+                    const float2 la1 = lut[ix.template mod_t<LMODE>(a1 + x)];
+                    const float2 la2 = lut[ix.template mod_t<LMODE>(a2 + xm)];
+                    const float2 lb1 = lut[ix.template mod_t<LMODE>(b1 + x)];
+                    const float2 lb2 = lut[ix.template mod_t<LMODE>(b2 + xm)];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, la1, la2, lb1, lb2);
+                    s0[x] = z.z1;
+                    s1[xm] = z.z2;
+                }
+            } else {       // rows 0 and N/2: pairs (yy, x) <-> (yy, N - x), x <= N/2
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const int yy = h ? N / 2 : 0;
+                    float2 *d = h ? s1 : s0;
+                    const uint32_t a1 = row_base(ba, yy, N, ix.L), b1 = row_base(bb, yy, N, ix.L);
+                    const float *T1 = T + (size_t)yy * N;
+                    for (int x = lane; x <= N / 2; x += 32) {
+                        const int xm = (N - x) & (N - 1);
+                        const float t1 = T1[x], t2 = T1[xm];
+                        const float2 la1 = lut[ix.template mod_t<LMODE>(a1 + x)];
+                        const float2 la2 = lut[ix.template mod_t<LMODE>(a1 + xm)];
+                        const float2 lb1 = lut[ix.template mod_t<LMODE>(b1 + x)];
+                        const float2 lb2 = lut[ix.template mod_t<LMODE>(b1 + xm)];
+                        const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, la1, la2, lb1, lb2);
+                        d[x] = z.z1;
+                        d[xm] = z.z2;
+                    }
                 }
             }
         }
@@ -565,6 +595,9 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const int npairs_total = (nsh + 1) / 2;
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
+    const float2 *lut_or_flat = lut;   // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
+    if (lut == nullptr)
+        HOLO_TRY(flat_lut(&lut_or_flat));
     const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
     const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
     for (int f = 0; f < n_frames; ++f) {
@@ -580,7 +613,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                 auto kern = ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
                           : ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2> : ospr_rows_a_kernel<N, LUT_GENERAL>;
                 const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
-                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut, ix,
+                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut_or_flat, ix,
                                 off_mod, p_mod, sf_first, np, last_has_b, w.buf));
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bits ? w.bt : nullptr, np, last_has_b};
