@@ -130,3 +130,14 @@ def test_product_package_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "holo_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_plan_queries(L):
+    assert L.holo_ospr_chunk_pairs(1024, 24) == 12          # C3: one L2-sized chunk of 12 pairs
+    assert L.holo_ospr_chunk_pairs(64, 7) == 4
+    assert L.holo_ospr_chunk_pairs(100, 7) == 0 and L.holo_ospr_chunk_pairs(64, 0) == 0
+    assert L.holo_gs_group_frames(1024, 64) == 16
+    assert L.holo_gs_group_frames(64, 3) == 3
+    assert L.holo_gs_group_frames(64, 0) == 0
+    assert L.holo_ospr_finalize_workspace_size() >= 592 * 5 * 8 + 4
+    assert L.holo_ospr_workspace_size(1024, 1, 24) >= L.holo_ospr_finalize_workspace_size()

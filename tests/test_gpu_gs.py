@@ -150,3 +150,16 @@ def test_gs_c4_full_size_sampled():
                 assert rel(mse[b, k], one["mse"]) <= REL_TOL, (b, k)
             tol = REL_TOL if k < 10 else 1e-3
             assert rel(mse[b, k], ref["mse"][k]) <= tol, (b, k, rel(mse[b, k], ref["mse"][k]))
+
+
+def test_gs_groups_bit_identical(monkeypatch):
+    """Frames are independent: splitting the batch into launch groups (a ragged last
+    group) changes no bit of any output; the plan query reports the group size."""
+    n, B, iters = 128, 5, 4
+    T = cuda_target(np.stack([blobs_target(100 + b, n, 4, 4.0, 10.0, Region.full(n)) for b in range(B)]))
+    lut = hb.lut_generate(LUT_SEED, 4096)
+    a = hb.gs_generate(T, iters, lut, levels=0)
+    monkeypatch.setenv("HOLO_GS_GROUP_BYTES", str(2 * n * n * 8))        # 2 frames per group
+    assert hb.gs_group_frames(n, B) == 2
+    b = hb.gs_generate(T, iters, lut, levels=0)
+    assert torch.equal(a.mse, b.mse) and torch.equal(a.holo, b.holo) and torch.equal(a.intensity, b.intensity)

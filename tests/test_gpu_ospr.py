@@ -216,3 +216,44 @@ def test_ospr_c5_sampled():
             check_bits(bits[f, s], h_re, n)
         assert rel(mse[f], oracle.mse_m1(I1, Ts[f], w.omega().as_tuple())) <= REL_TOL
         check_intensity(I[f], oracle.replay_from_bits(bits[f], n))
+
+
+def test_ospr_chunked_equals_single_chunk(monkeypatch):
+    """Several chunks of pairs (a ragged last one, the odd unpaired tail, accumulation
+    across chunks) give the same holograms as one chunk, and the same intensity up to
+    fp32 summation order; the plan query reports the chunk size used."""
+    n, S = 256, 11
+    T = cuda_target(blobs_target(4, n, 6, 4.0, 10.0, Region.upper_half(n)))
+    lut = hb.lut_generate(LUT_SEED, 10007)
+    one = hb.ospr_generate(T, S, lut, phase_offset=77)
+    assert hb.ospr_chunk_pairs(n, S) == (S + 1) // 2
+    monkeypatch.setenv("HOLO_OSPR_CHUNK_BYTES", str(2 * n * n * 8))       # 2 pairs per chunk
+    assert hb.ospr_chunk_pairs(n, S) == 2
+    many = hb.ospr_generate(T, S, lut, phase_offset=77)
+    assert torch.equal(one.bits, many.bits)
+    d = (one.intensity - many.intensity).abs().max().item() / one.intensity.abs().max().item()
+    assert d <= 1e-6
+    assert rel(one.mse.item(), many.mse.item()) <= 1e-6
+
+
+def test_ospr_graph_replay_bit_identical():
+    """The step captured into a CUDA graph (as bench.py times it) replays to exactly the
+    eager result."""
+    n, S = 128, 6
+    T = cuda_target(blobs_target(5, n, 6, 4.0, 10.0, Region.upper_half(n)))
+    lut = hb.lut_generate(LUT_SEED, 4099)
+    ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device="cuda")
+    eager = hb.ospr_generate(T, S, lut, workspace=ws)
+    out = hb.OsprResult(bits=torch.empty_like(eager.bits), intensity=torch.empty_like(eager.intensity),
+                        mse=torch.empty_like(eager.mse))
+    hb.ospr_generate(T, S, lut, workspace=ws, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        hb.ospr_generate(T, S, lut, workspace=ws, out=out)
+    out.bits.zero_()
+    out.intensity.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.bits, eager.bits) and torch.equal(out.intensity, eager.intensity)
+    assert torch.equal(out.mse, eager.mse)
