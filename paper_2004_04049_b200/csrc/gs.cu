@@ -244,7 +244,10 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                     state[rofs + t + R1 * r] = make_float2(v[r].x, -v[r].y);
                 break;
             }
-            float fe = 0.0f;
+            // g4 metrics: fp32 partial sums over this thread's E elements (unbiased rounding, a
+            // relative error ~1e-7 per partial), then fp64 across lanes, rows and frames
+            float fe = 0.0f, sI = 0.0f, sII = 0.0f, sIT = 0.0f;
+            const bool row_in = y >= om.row0 && y < om.row1, all_cols = om.col0 == 0 && om.col1 >= N;
 #pragma unroll
             for (int r = 0; r < E; ++r) {
                 const int x = t + R1 * r;
@@ -257,27 +260,22 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                 const float tt = tv[r];
                 const float d = __fsub_rn(amp, tt);
                 fe = __fmaf_rn(d, d, fe);
-                if (in_region(y, x, om)) {
-                    const double Id = I, t2 = __dmul_rn((double)tt, (double)tt);
-                    sums[0] = __dadd_rn(sums[0], Id);
-                    sums[1] = __fma_rn(Id, Id, sums[1]);
-                    sums[2] = __fma_rn(Id, t2, sums[2]);
+                if (row_in && (all_cols || (x >= om.col0 && x < om.col1))) {
+                    sI = __fadd_rn(sI, I);
+                    sII = __fmaf_rn(I, I, sII);
+                    sIT = __fmaf_rn(I, __fmul_rn(tt, tt), sIT);
                 }
                 if (MODE == GS_LAST || MODE == GS_STEP) {
                     if (inten != nullptr)
                         inten[rofs + x] = I;
                 }
-                if (MODE != GS_LAST) {
-                    float2 R;
-                    if (m2 > 0.0f) {
-                        const float sc = __fmul_rn(tt, rr);
-                        R = make_float2(__fmul_rn(X.x, sc), __fmul_rn(X.y, sc));   // no contraction into the IFFT
-                    } else {
-                        R = make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
-                    }
-                    v[r] = R;
-                }
+                if (MODE != GS_LAST)
+                    v[r] = m2 > 0.0f ? f2::mul(X, f2::bc(__fmul_rn(tt, rr)))   // R = T X / |X|
+                                     : make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
             }
+            sums[0] = (double)sI;
+            sums[1] = (double)sII;
+            sums[2] = (double)sIT;
             sums[3] = (double)fe;
             // warp reduction of the item's sums (lanes of all GPW rows of the item)
 #pragma unroll
