@@ -305,9 +305,8 @@ def run_gpu(args):
     alg_bytes = {                                                # DESIGN.md §7 table
         "ospr_rows_a": 4 * P + 8 * min(args.lut, 2 * np_l * P) + 8 * P * np_l,
         "ospr_cols": 16 * P * np_l + nsub_l * P / 8,
-        "ospr_bits": 2 * nsub_l * P / 8,
         "ospr_rows_c": 8 * P * np_l + 4 * P + (4 * P if nchunks > 1 else 0) * (nchunks - 1) / nchunks,
-        "ospr_finalize": 12 * P,
+        "ospr_finalize": 12 * P + 2 * (se - sb) * P / 8,             # + sign bytes -> packed holograms
     }
     dom = max((k for k in kern if k in alg_bytes), key=lambda k: kern[k]["total_ms"])
     per_launch = alg_bytes[dom]

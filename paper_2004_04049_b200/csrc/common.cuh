@@ -32,9 +32,8 @@ enum KernelId : int {
     K_LUT_GENERATE = 0,
     K_OSPR_ROWS_A,      // T x LUT for a sub-frame pair (Hermitian pairing) + row IFFT
     K_OSPR_COLS,        // column IFFT + sign quantise + bit pack + column FFT
-    K_OSPR_BITS,        // tile-major sign bytes -> row-major packed holograms
     K_OSPR_ROWS_C,      // row FFT + |.|^2 accumulate over the chunk's pairs
-    K_OSPR_FINALIZE,    // symmetrise/scale + MSE partial sums
+    K_OSPR_FINALIZE,    // symmetrise/scale + MSE + sign bytes -> packed holograms
     K_MSE_REDUCE,       // fixed-order reduction of partial sums -> MSE
     K_GS_ROWS_INIT,     // T x LUT (or R_in) + row IFFT
     K_GS_COLS,          // column IFFT + phase constraint + column FFT

@@ -14,7 +14,8 @@
 //                        over the chunk's pairs in registers; one RMW of the
 //                        frame accumulator A per chunk.
 //   finalize             I[k] = (A[k] + A[-k]) / 2 / N_SF  (= sum_s |F{h'_s}|^2 / N_SF,
-//                        DESIGN.md §5) and the fp64 MSE partial sums over Omega.
+//                        DESIGN.md §5), the fp64 MSE over Omega, and the packed
+//                        holograms (tile-major sign bytes -> row-major, R-8).
 //
 // All 1/sqrt(N) factors of Eqs. (1)-(2) are dropped inside the passes: a positive
 // scale does not change sign(Re H), and the forward scale 1/N^2 on |X|^2 is an
@@ -38,7 +39,7 @@ static holo_status flat_lut(const float2 **p)
     return HOLO_OK;
 }
 
-constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => deterministic sums)
+constexpr int kFinBlocks = 1184;  // finalize CTAs per frame (fixed => deterministic sums)
 constexpr int kFinThreads = 256;
 constexpr size_t kFinWsBytes = (size_t)kFinBlocks * 5 * sizeof(double) + 256;   // partial sums + ticket
 
@@ -253,7 +254,7 @@ struct OsprColBody {
         // bits r of words [f][t'][0..7]; a task gathers 8 rows r = 8*rb .. 8*rb+7 of one t' as
         // an 8x8 bit matrix (byte 7-c = column c) and transposes it into the 8 row bytes.  The
         // bytes go to the tile-major staging layout bt[sub-frame][ct][y] (a warp writes 32
-        // consecutive rows = one sector); ospr_bits_transpose_kernel makes them row-major.
+        // consecutive rows = one sector); the finalize kernel makes them row-major.
         if (a.bits != nullptr) {
             constexpr int RG = E < 8 ? 1 : E / 8, RPG = E < 8 ? E : 8, TASKS = 2 * R1 * RG;
 #pragma unroll 1
@@ -286,16 +287,21 @@ struct OsprColBody {
 };
 
 // Tile-major sign bytes bt[q][ct][y] (ct < N/8, y < N) -> row-major packed holograms
-// out[q][y][ct] (R-8).  Block (y-block, q): YB rows of one sub-frame through shared memory;
+// out[q][y][ct] (R-8), one block of YB rows of sub-frame q per CTA, through shared memory;
 // 32-bit words on both global sides when N >= 32 (every thread's loads in flight at once).
+// Run by the extra CTAs of ospr_finalize_kernel (256 threads).
 template <int N>
-__global__ void __launch_bounds__(256)
-ospr_bits_transpose_kernel(const uint8_t *__restrict__ bt, uint8_t *__restrict__ out)
+struct BitsT {
+    static constexpr int C = N / 8, YB = N < 32 ? N : 32, BLOCKS_PER_Q = N / YB;
+};
+
+template <int N>
+__device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__ bt, uint8_t *__restrict__ out, int q,
+                                                     int yblk)
 {
-    HOLO_PDL_ENTRY();
-    constexpr int C = N / 8, YB = N < 32 ? N : 32;
+    constexpr int C = BitsT<N>::C, YB = BitsT<N>::YB;
     __shared__ __align__(16) uint8_t sm[C][YB + 4];
-    const int q = blockIdx.y, y0 = blockIdx.x * YB;
+    const int y0 = yblk * YB;
     const uint8_t *src = bt + (size_t)q * C * N + y0;
     uint8_t *dst = out + ((size_t)q * N + y0) * C;
     if constexpr (N >= 32) {
@@ -454,21 +460,28 @@ __device__ __forceinline__ double mse_from_sums(const double *o, double inv_coun
 // partial sums (sum I, sum I^2, sum I T^2, sum T^2, sum T^4) over Omega, one slot per CTA.
 // With mse != NULL the last CTA to finish (atomic ticket on *counter, which the host zeroes
 // before the launch and the last CTA re-zeroes) reduces the slots in CTA order -- a fixed
-// order, so the MSE is deterministic -- and writes R-12.
+// order, so the MSE is deterministic -- and writes R-12.  CTAs fb.. of the grid instead
+// transpose the frame's nq sub-frames of tile-major sign bytes into packed holograms.
+template <int N>
 __global__ void __launch_bounds__(kFinThreads)
-ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T, int n, int symmetrise,
-                     float scale, float *out, holo_region om, double *__restrict__ parts, unsigned *counter,
-                     double inv_count, double *__restrict__ mse)
+ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T, int symmetrise, float scale,
+                     float *out, holo_region om, double *__restrict__ parts, unsigned *counter, double inv_count,
+                     double *__restrict__ mse, int fb, const uint8_t *__restrict__ bt, uint8_t *__restrict__ bits)
 {
     HOLO_PDL_ENTRY();
-    const int P = n * n;
+    if ((int)blockIdx.x >= fb) {
+        const int j = (int)blockIdx.x - fb;
+        bits_transpose_block<N>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
+        return;
+    }
+    constexpr int P = N * N, LOG = fft::ilog2(N);
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P; k += gridDim.x * blockDim.x) {
-        const int y = k / n, x = k - y * n;
+    for (int k = blockIdx.x * kFinThreads + threadIdx.x; k < P; k += fb * kFinThreads) {
+        const int y = k >> LOG, x = k & (N - 1);
         float I;
         if (symmetrise) {
-            const int km = ((n - y) & (n - 1)) * n + ((n - x) & (n - 1));
+            const int km = (((N - y) & (N - 1)) << LOG) + ((N - x) & (N - 1));
             I = (__ldg(acc + k) + __ldg(acc + km)) * scale;
         } else {
             I = __ldg(acc + k) * scale;
@@ -491,14 +504,14 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
     __shared__ int last;
     if (threadIdx.x == 0) {
         __threadfence();                                   // this CTA's slot before its ticket
-        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        last = atomicAdd(counter, 1u) == (unsigned)fb - 1;
     }
     __syncthreads();
     if (!last)
         return;
     __threadfence();
     double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+    for (int b = threadIdx.x; b < fb; b += blockDim.x)
         for (int i = 0; i < 5; ++i)
             t[i] += __ldcg(parts + (size_t)b * 5 + i);
     __shared__ double o[5];
@@ -550,7 +563,7 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     const size_t o_parts = off;
     off = align256(off + kFinWsBytes);
     const size_t o_bt = off;
-    off = align256(off + (size_t)2 * chunk * P / 8);
+    off = align256(off + (size_t)(2 * ((n_sub + 1) / 2)) * P / 8);   // sign bytes of a frame's sub-frames
     if (w) {
         w->buf = (float2 *)(base + o_buf);
         w->acc = (float *)(base + o_acc);
@@ -563,14 +576,16 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
 
 static int fin_grid(int n)
 {
-    const int want = (n * n + kFinThreads - 1) / kFinThreads;
+    const int want = (n * n + 4 * kFinThreads - 1) / (4 * kFinThreads);   // >= 4 pixels per thread
     return want < kFinBlocks ? want : kFinBlocks;
 }
 
-holo_status finalize_frame(const float *acc, const float *T, int n, int symmetrise, float scale,
-                           float *out, holo_region om, double *parts, double *mse, cudaStream_t s)
+// Finalize one frame (and, if bits != NULL, transpose its nq sub-frames of sign bytes).
+template <int N>
+holo_status finalize_frame(const float *acc, const float *T, int symmetrise, float scale, float *out, holo_region om,
+                           double *parts, double *mse, const uint8_t *bt, uint8_t *bits, int nq, cudaStream_t s)
 {
-    const int grid = fin_grid(n);
+    const int fb = fin_grid(N);
     unsigned *counter = reinterpret_cast<unsigned *>(parts + (size_t)kFinBlocks * 5);
     const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
     if (mse) {
@@ -578,8 +593,9 @@ holo_status finalize_frame(const float *acc, const float *T, int n, int symmetri
         if (e != cudaSuccess)
             return cuda_status(e, "cudaMemsetAsync(finalize ticket)");
     }
-    return launch(K_OSPR_FINALIZE, ospr_finalize_kernel, dim3(grid), dim3(kFinThreads), 0, s, acc, T, n, symmetrise,
-                  scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse);
+    const int nbt = bits ? nq * BitsT<N>::BLOCKS_PER_Q : 0;
+    return launch(K_OSPR_FINALIZE, ospr_finalize_kernel<N>, dim3(fb + nbt), dim3(kFinThreads), 0, s, acc, T,
+                  symmetrise, scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse, fb, bt, bits);
 }
 
 template <int N>
@@ -606,7 +622,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const int np = (npairs_total - c0) < chunk ? (npairs_total - c0) : chunk;
             const int last_sa = sf_begin + 2 * (c0 + np - 1);
             const int last_has_b = (last_sa + 1) < sf_end;
-            uint8_t *bits = holo_bits ? holo_bits + ((size_t)f * nsh + 2 * (size_t)c0) * (P / 8) : nullptr;
+            uint8_t *bt = holo_bits ? w.bt + 2 * (size_t)c0 * (P / 8) : nullptr;
             {
                 using RA = RowA<N>;
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
@@ -616,13 +632,8 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                 HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut_or_flat, ix,
                                 off_mod, p_mod, sf_first, np, last_has_b, w.buf));
             }
-            typename OsprColBody<N>::Args ca{tw, w.buf, bits ? w.bt : nullptr, np, last_has_b};
+            typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
-            if (bits) {
-                constexpr int YB = N < 32 ? N : 32;
-                HOLO_TRY(launch(K_OSPR_BITS, ospr_bits_transpose_kernel<N>, dim3(N / YB, 2 * np - (last_has_b ? 0 : 1)),
-                                dim3(256), 0, s, (const uint8_t *)w.bt, bits));
-            }
             {
                 using RP = RowPipe<N>;
                 constexpr size_t smem =
@@ -633,8 +644,9 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             }
         }
         const float scale = full ? 0.5f / (float)n_sub : 0.5f;
-        HOLO_TRY(finalize_frame(w.acc, Tf, N, 1, scale, intensity + (size_t)f * P, om, w.parts,
-                                (full && mse) ? mse + f : nullptr, s));
+        HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
+                                   (full && mse) ? mse + f : nullptr, w.bt,
+                                   holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr, nsh, s));
     }
     return HOLO_OK;
 }
@@ -734,9 +746,28 @@ extern "C" holo_status holo_ospr_finalize(const float *target, const float *inte
             return set_error(HOLO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
     }
     const size_t P = (size_t)n * n;
-    for (int f = 0; f < n_frames; ++f)
-        HOLO_TRY(finalize_frame(intensity_sum + f * P, target + f * P, n, 0, 1.0f / (float)n_sub,
-                                intensity_mean + f * P, omega, (double *)ws, mse ? mse + f : nullptr,
-                                (cudaStream_t)stream));
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int f = 0; f < n_frames; ++f) {
+        const float *a = intensity_sum + f * P, *t = target + f * P;
+        float *o = intensity_mean + f * P;
+        double *m = mse ? mse + f : nullptr, *parts = (double *)ws;
+#define HOLO_FIN_CASE(NN)                                                                                  \
+    case NN:                                                                                               \
+        HOLO_TRY(finalize_frame<NN>(a, t, 0, 1.0f / (float)n_sub, o, omega, parts, m, nullptr, nullptr, 0, s)); \
+        break;
+        switch (n) {
+            HOLO_FIN_CASE(16)
+            HOLO_FIN_CASE(32)
+            HOLO_FIN_CASE(64)
+            HOLO_FIN_CASE(128)
+            HOLO_FIN_CASE(256)
+            HOLO_FIN_CASE(512)
+            HOLO_FIN_CASE(1024)
+            HOLO_FIN_CASE(2048)
+        default:
+            return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
+        }
+#undef HOLO_FIN_CASE
+    }
     return HOLO_OK;
 }

@@ -21,7 +21,7 @@
 namespace holo {
 
 const char *const kKernelNames[K_NUM_KERNELS] = {
-    "lut_generate", "ospr_rows_a", "ospr_cols", "ospr_bits", "ospr_rows_c", "ospr_finalize", "mse_reduce",
+    "lut_generate", "ospr_rows_a", "ospr_cols", "ospr_rows_c", "ospr_finalize", "mse_reduce",
     "gs_rows_init", "gs_cols",     "gs_rows",   "fft_rows",    "fft_cols",      "randomise",
 };
 
