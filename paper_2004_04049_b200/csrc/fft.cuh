@@ -236,8 +236,16 @@ struct Twiddles {
 // and synchronise with __syncwarp(), so warps run independently; WS = false: the
 // threads span warps (column tiles) and every thread of the CTA must call this
 // together (__syncthreads()).
-template <int N, bool INV, int IL, bool WS, class TwSrc>
-__device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *sm, int t, const TwSrc &tws)
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// `after_exchange` runs once every value has been read back from the exchange buffer and
+// consumed (pass-2 twiddles applied), before the pass-2 DFT: the buffer may be refilled
+// from there on (row pipelines issue their next TMA load into it, WS = true only).
+template <int N, bool INV, int IL, bool WS, class TwSrc, class Hook = NoHook>
+__device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *sm, int t, const TwSrc &tws,
+                                              const Hook &after_exchange = Hook())
 {
     using P = Plan<N>;
     constexpr int R1 = P::R1, R2 = P::R2, Q = P::Q;
@@ -271,6 +279,7 @@ __device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *s
         }
         v[r] = x;
     }
+    after_exchange();
     Dft<R2, 1, INV>::run(v);
 }
 
@@ -292,6 +301,14 @@ __device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, in
                                          const float2 *__restrict__ twp)
 {
     fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwGlobal<N>{twp + Plan<N>::TW_OFFSET + t});
+}
+
+// Twiddles from the pool, with a hook after the exchange (see fft2pass_impl).
+template <int N, bool INV, int IL, bool WS, class Hook>
+__device__ __forceinline__ void fft2pass_hook(float2 (&v)[Plan<N>::E], float2 *sm, int t, const float2 *__restrict__ twp,
+                                              const Hook &after_exchange)
+{
+    fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwGlobal<N>{twp + Plan<N>::TW_OFFSET + t}, after_exchange);
 }
 
 // Twiddles prepared by the caller (Twiddles<N>::load once per role).

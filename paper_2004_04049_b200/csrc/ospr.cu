@@ -131,7 +131,7 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
                 const uint32_t b1 = row_base(bb, y, N, ix.L), b2 = row_base(bb, ym, N, ix.L);
                 const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
                 constexpr int M = N < 32 ? 1 : N / 32;
-#pragma unroll 8
+#pragma unroll 16
                 for (int m = 0; m < M; ++m) {
                     const int x = lane + 32 * m;
                     if (N < 32 && x >= N)
@@ -340,73 +340,86 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
 }
 
 // ---- pass C: row FFT + |X|^2 summed over the chunk's pairs --------------------------------------
-// Row pipeline (passes.cuh): each warp owns whole row groups y and streams the np pair
-// rows (y, p), p = 0..np-1, through its two ring slots, summing |X|^2 / N^2 over p in
-// registers (fixed order => deterministic), then one read-modify-write of the frame
-// accumulator A per row and chunk.
+// One CTA = one row group y (GPW rows) at a time, two warps splitting the chunk's pairs.
+// Each warp streams its pair rows (y, p) through ONE shared-memory slot: the 1D TMA load of
+// the next pair row is issued as soon as the current transform has read its exchange back,
+// so it overlaps pass 2 and the |X|^2 accumulation.  Small CTAs (two warps, ~21 KB) let a
+// whole N = 1024 frame's row groups be resident in one wave, instead of the 1.15 waves
+// (58 % efficiency) of four-warp CTAs.  The halves are summed in a fixed order
+// (deterministic), then one read-modify-write of the frame accumulator A per row and chunk.
 template <int N>
-__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+struct RowC {
+    using P = fft::Plan<N>;
+    static constexpr int GPW = 32 / P::T, NGRP = N / GPW;
+    static constexpr uint32_t IN_BYTES = (uint32_t)GPW * N * 8;
+    static constexpr uint32_t XCH_BYTES = (uint32_t)GPW * P::SMEM * 8;
+    static constexpr uint32_t SLOT = ((XCH_BYTES > IN_BYTES ? XCH_BYTES : IN_BYTES) + 127) / 128 * 128;
+    static constexpr size_t RED = (size_t)GPW * N * sizeof(float);
+    static constexpr size_t SMEM = 2 * (size_t)SLOT + RED + 2 * sizeof(uint64_t);
+};
+
+template <int N>
+__global__ void __launch_bounds__(64)
 ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
                    float *__restrict__ acc, int accumulate)
 {
     HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
-    using RP = RowPipe<N>;
-    constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW, GPC = RP::WPC / 2;
-    static_assert(RP::WPC % 2 == 0, "two warps (pair halves) per row group");
+    using RC = RowC<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RC::GPW, NGRP = RC::NGRP;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const WarpRing ring = make_ring<RP::SLOT_C, RP::WPC>(smem_raw);
-    float *red = reinterpret_cast<float *>(smem_raw + ring_smem<RP::SLOT_C, RP::WPC>());   // [GPC][GPW*N]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
-    const int lg = warp >> 1, half = warp & 1;
+    const int half = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)half * RC::SLOT);
+    float *red = reinterpret_cast<float *>(smem_raw + 2 * (size_t)RC::SLOT);              // [GPW*N]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + 2 * (size_t)RC::SLOT + RC::RED) + half;
     const int hp = (npairs + 1) / 2;                     // pairs of half 0; half 1 gets the rest
     const int p0 = half * hp, p1 = half ? npairs : hp;
-    const int stride = gridDim.x * GPC;
     auto src = [&](int gg, int p) { return buf + ((size_t)p * N + (size_t)gg * GPW) * N; };
-    fft::Twiddles<N, false> twr;                          // pool twiddles: keeps registers for a[]
-    twr.load(tw, t);
-    int grp = blockIdx.x * GPC + lg;
-    if (lane == 0 && grp < NGRP && p0 < p1) {
-        tma::mbar_arrive_expect_tx(&ring.bars[0], RP::IN_BYTES);
-        tma::load_1d(ring.slot(0), src(grp, p0), RP::IN_BYTES, &ring.bars[0]);
+    if (lane == 0) {
+        tma::mbar_init(bar, 1);
+        tma::fence_mbar_init();
     }
-    int k = 0;
-    #pragma unroll 1   // one copy of the transform code (instruction cache)
-    for (; grp < NGRP; grp += stride) {
+    __syncwarp();
+    int grp = blockIdx.x;
+    if (lane == 0 && grp < NGRP && p0 < p1) {
+        tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
+        tma::load_1d(sl, src(grp, p0), RC::IN_BYTES, bar);
+    }
+    uint32_t k = 0;
+    #pragma unroll 1
+    for (; grp < NGRP; grp += gridDim.x) {
         float a[E];
 #pragma unroll
         for (int r = 0; r < E; ++r)
             a[r] = 0.0f;
         #pragma unroll 1   // one copy of the transform code (instruction cache)
         for (int p = p0; p < p1; ++p, ++k) {
-            const int s = k & 1;
-            const bool more = (p + 1 < p1) || (grp + stride < NGRP);
-            if (lane == 0 && more) {
-                const float2 *nx = (p + 1 < p1) ? src(grp, p + 1) : src(grp + stride, p0);
-                tma::mbar_arrive_expect_tx(&ring.bars[s ^ 1], RP::IN_BYTES);
-                tma::load_1d(ring.slot(s ^ 1), nx, RP::IN_BYTES, &ring.bars[s ^ 1]);
-            }
-            tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
-            float2 *sl = reinterpret_cast<float2 *>(ring.slot(s));
+            tma::mbar_wait(bar, k & 1u);
             float2 v[E];
 #pragma unroll
             for (int m = 0; m < E; ++m)
                 v[m] = sl[g * N + t + R1 * m];
-            fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);
+            const bool more = (p + 1 < p1) || (grp + (int)gridDim.x < NGRP);
+            const float2 *nx = (p + 1 < p1) ? src(grp, p + 1) : src(grp + gridDim.x, p0);
+            fft::fft2pass_hook<N, false, 1, true>(v, sl + g * P::SMEM, t, tw, [&] {
+                __syncwarp();                            // every lane has consumed the exchange
+                if (lane == 0 && more) {
+                    tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
+                    tma::load_1d(sl, nx, RC::IN_BYTES, bar);
+                }
+            });
 #pragma unroll
             for (int r = 0; r < E; ++r)
-                a[r] += v[r].x * v[r].x + v[r].y * v[r].y;
-            tma::fence_proxy_async_smem();
-            __syncwarp();
+                a[r] = __fmaf_rn(v[r].x, v[r].x, __fmaf_rn(v[r].y, v[r].y, a[r]));
         }
         // combine the two halves (half 0 + half 1, fixed order) and update A
-        float *rg = red + (size_t)lg * GPW * N + g * N;
+        float *rg = red + g * N;
         if (half == 1) {
 #pragma unroll
             for (int r = 0; r < E; ++r)
                 rg[t + R1 * r] = a[r];
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + lg) : "memory");
+        __syncthreads();
         if (half == 0) {
             constexpr float inv_p = 1.0f / ((float)N * (float)N);   // exact power of two
             float *o = acc + ((size_t)grp * GPW + g) * N;
@@ -416,7 +429,7 @@ ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf
                 o[t + R1 * r] = accumulate ? o[t + R1 * r] + val : val;
             }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + lg) : "memory");
+        __syncthreads();
     }
 }
 
@@ -635,11 +648,9 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
             {
-                using RP = RowPipe<N>;
-                constexpr size_t smem =
-                    ring_smem<RP::SLOT_C, RP::WPC>() + (size_t)(RP::WPC / 2) * RP::GPW * N * sizeof(float);
-                const int grid = pipe_grid(ospr_rows_c_kernel<N>, RP::WPC * 32, smem, 2 * (N / RP::GPW), RP::WPC);
-                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                using RC = RowC<N>;
+                const int grid = pipe_grid(ospr_rows_c_kernel<N>, 64, RC::SMEM, RC::NGRP, 1);
+                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(grid), dim3(64), RC::SMEM, s, tw,
                                 (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0));
             }
         }
