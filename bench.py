@@ -351,6 +351,16 @@ def run_gpu(args):
             tm, _ = timed_loop(st, max(3, args.steps // 2), 2, world, flush)
             sweep[str(L)] = {"sub_frames_per_s": S * max(3, args.steps // 2) / (tm / 1e3),
                              "ms_per_step": tm / max(3, args.steps // 2), "mse": float(out.mse.item())}
+        # no pool at all -- SplitMix64 + R-5 per draw in pass A (bit-identical
+        # to the full-length pool above, which it replaces: the paper's memory-vs-compute trade-off)
+        def prng_step():
+            hb.ospr_generate(T, S, prng_seed=LUT_SEED, workspace=ws, out=out)
+        st = graphed(prng_step, use_graph)
+        ks = max(3, args.steps // 2)
+        tm, _ = timed_loop(st, ks, 2, world, flush)
+        sweep["prng"] = {"sub_frames_per_s": S * ks / (tm / 1e3), "ms_per_step": tm / ks,
+                         "mse": float(out.mse.item()),
+                         "what": "phases drawn on the fly (holo_ospr_generate_prng), no LUT"}
         result["lut_sweep"] = sweep
         del big
 

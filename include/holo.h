@@ -140,6 +140,21 @@ holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames,
                                float *intensity, double *mse, holo_region omega, void *ws,
                                size_t ws_bytes, holo_stream stream);
 
+/* OSPR with the phases drawn on the fly instead of read from a pool (SURVEY.md
+ * §8(f) f2; the paper's memory-vs-compute trade-off):
+ * the phase of global draw index g = phase_offset + (f*n_sub + s)*n^2 + p is
+ * recipe R-5 of the high word of SplitMix64(seed, g) -- entry g of
+ * holo_lut_generate(seed, L) for every L > g -- evaluated in pass A for every
+ * pixel, with no wrap.  Results are therefore bit-identical to
+ * holo_ospr_generate with a pool generated from the same seed and longer than
+ * every draw index ("a LUT the same length as the number of random
+ * numbers").  Every other argument, output and error as
+ * holo_ospr_generate. */
+holo_status holo_ospr_generate_prng(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
+                                    uint64_t seed, uint64_t phase_offset, int32_t sf_begin,
+                                    int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse,
+                                    holo_region omega, void *ws, size_t ws_bytes, holo_stream stream);
+
 /* Mean intensity and MSE from a summed intensity (after the caller's
  * cross-rank sum of holo_ospr_generate partial sums): intensity_mean =
  * intensity_sum / n_sub (in place allowed), mse as step a7.
@@ -182,7 +197,7 @@ holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, 
 size_t holo_gs_workspace_size(int32_t n, int32_t batch, int32_t iters);
 
 /* Plan query (instrumentation): frames per launch group of holo_gs_generate(n,
- * batch, ...) (HOLO_GS_GROUP_BYTES overrides the 128 MiB budget);
+ * batch, ...) (HOLO_GS_GROUP_BYTES overrides the 512 MiB budget);
  * 0 for invalid n or batch. */
 int32_t holo_gs_group_frames(int32_t n, int32_t batch);
 

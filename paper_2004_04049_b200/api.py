@@ -101,8 +101,9 @@ def gs_group_frames(n: int, batch: int) -> int:
 def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] = None, phase_offset: int = 0,
                   sf_range: Optional[Tuple[int, int]] = None, want_bits: bool = True, want_mse: bool = True,
                   omega: Optional[Sequence[int]] = None, workspace: Optional[torch.Tensor] = None,
-                  out: Optional[OsprResult] = None) -> OsprResult:
-    """OSPR over target [F][N][N] (or [N][N]); see holo_ospr_generate."""
+                  out: Optional[OsprResult] = None, prng_seed: Optional[int] = None) -> OsprResult:
+    """OSPR over target [F][N][N] (or [N][N]); see holo_ospr_generate.  With prng_seed the
+    phases are drawn on the fly (holo_ospr_generate_prng) and `lut` must be None."""
     _need(target, torch.float32, "target")
     t3 = target if target.dim() == 3 else target.unsqueeze(0)
     F, n, _ = t3.shape
@@ -118,6 +119,13 @@ def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] 
     need = ospr_workspace_bytes(n, F, n_sub)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    if prng_seed is not None:
+        if lut is not None:
+            raise ValueError("pass either lut or prng_seed, not both")
+        check(lib().holo_ospr_generate_prng(t3.data_ptr(), n, F, n_sub, prng_seed & 0xFFFFFFFFFFFFFFFF, phase_offset,
+                                            b, e, _ptr(out.bits), out.intensity.data_ptr(), _ptr(out.mse),
+                                            _region(om), workspace.data_ptr(), workspace.numel(), _stream(dev)))
+        return out
     lp, L = _lut_args(lut)
     check(lib().holo_ospr_generate(t3.data_ptr(), n, F, n_sub, lp, L, phase_offset, b, e, _ptr(out.bits),
                                    out.intensity.data_ptr(), _ptr(out.mse), _region(om), workspace.data_ptr(),

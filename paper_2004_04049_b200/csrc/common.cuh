@@ -176,7 +176,7 @@ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2
 // hardware divide: L >= N needs at most one subtraction; a power-of-two L is a mask;
 // otherwise Lemire's fastmod (exact for 32-bit operands).  An empty pool (N_LUT = 0,
 // R-6) is indexed as the one-entry pool {1 + 0i} (L = 1, mask 0).
-enum LutMode : int { LUT_WRAP = 0, LUT_POW2 = 1, LUT_GENERAL = 2 };
+enum LutMode : int { LUT_WRAP = 0, LUT_POW2 = 1, LUT_GENERAL = 2, LUT_PRNG = 3 /* no pool: ospr.cu */ };
 struct LutIndexer {
     uint32_t L;       // N_LUT (> 0)
     uint32_t mode;    // LutMode

@@ -344,7 +344,7 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 static int gs_group(int n, int batch)
 {
     const size_t frame = (size_t)n * n * sizeof(float2);
-    size_t budget = 128ull << 20;  // frames per launch group (measured: larger groups amortise pass tails)
+    size_t budget = 512ull << 20;  // frames per launch group (measured: larger groups amortise pass tails)
     if (const char *e = getenv("HOLO_GS_GROUP_BYTES"))
         budget = strtoull(e, nullptr, 10);
     long g = (long)(budget / frame);

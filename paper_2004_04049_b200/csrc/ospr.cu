@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "passes.cuh"
+#include "phase.cuh"
 
 namespace holo {
 
@@ -96,15 +97,53 @@ struct RowA {
     static constexpr size_t SMEM = (size_t)WPC * SLOT;
 };
 
+// The phase source of pass A: the LUT (modes LUT_WRAP / LUT_POW2 / LUT_GENERAL, index
+// (off + s N^2 + p) mod L) or, in mode LUT_PRNG, SplitMix64 + recipe R-5 evaluated per
+// draw (index off + s N^2 + p, no wrap): bit-identical to a LUT longer than every index.
+struct PhaseSrc {
+    const float2 *lut;
+    LutIndexer ix;
+    uint32_t off_mod, p_mod;   // phase_offset mod L, N^2 mod L
+    uint64_t seed, off;        // LUT_PRNG: stream seed, phase_offset
+};
+
+template <int N, int LMODE>
+struct PhaseRows {
+    using Base = typename std::conditional<LMODE == LUT_PRNG, uint64_t, uint32_t>::type;
+    // draw index of pixel 0 of global sub-frame s (mod L for the LUT)
+    static __device__ __forceinline__ Base subframe(const PhaseSrc &ps, uint64_t s)
+    {
+        if constexpr (LMODE == LUT_PRNG)
+            return ps.off + s * (uint64_t)N * N;
+        else
+            return subframe_base(ps.off_mod, s, ps.p_mod, ps.ix.L);
+    }
+    static __device__ __forceinline__ Base row(const PhaseSrc &ps, Base sb, int y)
+    {
+        if constexpr (LMODE == LUT_PRNG)
+            return sb + (uint64_t)y * N;
+        else
+            return row_base(sb, y, N, ps.ix.L);
+    }
+    static __device__ __forceinline__ float2 at(const PhaseSrc &ps, Base rb, int x)
+    {
+        if constexpr (LMODE == LUT_PRNG)
+            return prng_phase(ps.seed, rb + (uint64_t)x);
+        else
+            return ps.lut[ps.ix.template mod_t<LMODE>(rb + (uint32_t)x)];
+    }
+};
+
 template <int N, int LMODE>
 __global__ void __launch_bounds__(RowA<N>::WPC * 32)
-ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut,
-                   LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t sf_first, int npairs,
-                   int last_pair_has_b, float2 *__restrict__ buf)
+ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
+                   int npairs, int last_pair_has_b, float2 *__restrict__ buf)
 {
     HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
     using RA = RowA<N>;
+    using PR = PhaseRows<N, LMODE>;
+    using Base = typename PR::Base;
     constexpr int R1 = P::R1, E = P::E, GPW = RA::GPW, IPU = RA::IPU;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
@@ -116,8 +155,8 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
     for (int u = blockIdx.x * RA::WPC + warp; u < nunits; u += gridDim.x * RA::WPC) {
         const int pair = u / RA::UNITS_PER_PAIR, k0 = (u % RA::UNITS_PER_PAIR) * IPU;
         const bool has_b = (pair < npairs - 1) || last_pair_has_b;
-        const uint32_t ba = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair, p_mod, ix.L);
-        const uint32_t bb = subframe_base(off_mod, sf_first + 2 * (uint64_t)pair + 1, p_mod, ix.L);
+        const Base ba = PR::subframe(ps, sf_first + 2 * (uint64_t)pair);
+        const Base bb = PR::subframe(ps, sf_first + 2 * (uint64_t)pair + 1);
         const float bsc = has_b ? 1.0f : 0.0f;   // an absent sub-frame b contributes R_b = 0
         // build Z: row slot 2i holds row y, slot 2i+1 its mirror row ym (padded stride P::SMEM).
         // Rows 0 and N/2 are their own mirrors: their pairs are x <-> N - x, x in [0, N/2].
@@ -127,22 +166,19 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
             float2 *s0 = sl + (size_t)j * P::SMEM, *s1 = s0 + P::SMEM;
             if (k > 0) {   // pixel pairs (k, x) <-> (N - k, N - x), x < N: N/32 per lane
                 const int y = k, ym = N - k;
-                const uint32_t a1 = row_base(ba, y, N, ix.L), a2 = row_base(ba, ym, N, ix.L);
-                const uint32_t b1 = row_base(bb, y, N, ix.L), b2 = row_base(bb, ym, N, ix.L);
+                const Base a1 = PR::row(ps, ba, y), a2 = PR::row(ps, ba, ym);
+                const Base b1 = PR::row(ps, bb, y), b2 = PR::row(ps, bb, ym);
                 const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
                 constexpr int M = N < 32 ? 1 : N / 32;
-#pragma unroll 16
+#pragma unroll (LMODE == LUT_PRNG ? 2 : 16)
                 for (int m = 0; m < M; ++m) {
                     const int x = lane + 32 * m;
                     if (N < 32 && x >= N)
                         break;
                     const int xm = (N - x) & (N - 1);
                     const float t1 = T1[x], t2 = T2[xm];
-                    const float2 la1 = lut[ix.template mod_t<LMODE>(a1 + x)];
-                    const float2 la2 = lut[ix.template mod_t<LMODE>(a2 + xm)];
-                    const float2 lb1 = lut[ix.template mod_t<LMODE>(b1 + x)];
-                    const float2 lb2 = lut[ix.template mod_t<LMODE>(b2 + xm)];
-                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, la1, la2, lb1, lb2);
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a2, xm),
+                                           PR::at(ps, b1, x), PR::at(ps, b2, xm));
                     s0[x] = z.z1;
                     s1[xm] = z.z2;
                 }
@@ -151,16 +187,13 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
                 for (int h = 0; h < 2; ++h) {
                     const int yy = h ? N / 2 : 0;
                     float2 *d = h ? s1 : s0;
-                    const uint32_t a1 = row_base(ba, yy, N, ix.L), b1 = row_base(bb, yy, N, ix.L);
+                    const Base a1 = PR::row(ps, ba, yy), b1 = PR::row(ps, bb, yy);
                     const float *T1 = T + (size_t)yy * N;
                     for (int x = lane; x <= N / 2; x += 32) {
                         const int xm = (N - x) & (N - 1);
                         const float t1 = T1[x], t2 = T1[xm];
-                        const float2 la1 = lut[ix.template mod_t<LMODE>(a1 + x)];
-                        const float2 la2 = lut[ix.template mod_t<LMODE>(a1 + xm)];
-                        const float2 lb1 = lut[ix.template mod_t<LMODE>(b1 + x)];
-                        const float2 lb2 = lut[ix.template mod_t<LMODE>(b1 + xm)];
-                        const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, la1, la2, lb1, lb2);
+                        const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a1, xm),
+                                               PR::at(ps, b1, x), PR::at(ps, b1, xm));
                         d[x] = z.z1;
                         d[xm] = z.z2;
                     }
@@ -613,8 +646,8 @@ holo_status finalize_frame(const float *acc, const float *T, int symmetrise, flo
 
 template <int N>
 static holo_status ospr_run(const float2 *tw, const float *target, int n_frames, int n_sub, const float2 *lut, uint64_t n_lut,
-                            uint64_t phase_offset, int sf_begin, int sf_end, uint8_t *holo_bits,
-                            float *intensity, double *mse, holo_region om, void *ws, cudaStream_t s)
+                            bool prng, uint64_t seed, uint64_t phase_offset, int sf_begin, int sf_end,
+                            uint8_t *holo_bits, float *intensity, double *mse, holo_region om, void *ws, cudaStream_t s)
 {
     constexpr size_t P = (size_t)N * N;
     OsprWs w;
@@ -623,12 +656,15 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const int nsh = sf_end - sf_begin;
     const int npairs_total = (nsh + 1) / 2;
     const bool full = (sf_begin == 0 && sf_end == n_sub);
-    const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
-    const float2 *lut_or_flat = lut;   // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
-    if (lut == nullptr)
-        HOLO_TRY(flat_lut(&lut_or_flat));
-    const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
-    const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
+    PhaseSrc ps;
+    ps.ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
+    ps.lut = lut;                      // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
+    if (lut == nullptr && !prng)
+        HOLO_TRY(flat_lut(&ps.lut));
+    ps.off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
+    ps.p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
+    ps.seed = seed;
+    ps.off = phase_offset;
     for (int f = 0; f < n_frames; ++f) {
         const float *Tf = target + (size_t)f * P;
         for (int c0 = 0; c0 < npairs_total; c0 += chunk) {
@@ -639,11 +675,13 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             {
                 using RA = RowA<N>;
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                auto kern = ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
-                          : ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2> : ospr_rows_a_kernel<N, LUT_GENERAL>;
+                auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG>
+                          : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
+                          : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2>
+                                                   : ospr_rows_a_kernel<N, LUT_GENERAL>;
                 const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
-                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, lut_or_flat, ix,
-                                off_mod, p_mod, sf_first, np, last_has_b, w.buf));
+                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, ps, sf_first,
+                                np, last_has_b, w.buf));
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
@@ -698,11 +736,10 @@ extern "C" int32_t holo_ospr_chunk_pairs(int32_t n, int32_t n_sub)
     return ospr_chunk_pairs(n, n_sub);
 }
 
-extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
-                                          const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset,
-                                          int32_t sf_begin, int32_t sf_end, uint8_t *holo_bits,
-                                          float *intensity, double *mse, holo_region omega, void *ws,
-                                          size_t ws_bytes, holo_stream stream)
+static holo_status ospr_entry(const float *target, int32_t n, int32_t n_frames, int32_t n_sub, const holo_c64 *lut,
+                              uint64_t n_lut, bool prng, uint64_t seed, uint64_t phase_offset, int32_t sf_begin,
+                              int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse, holo_region omega,
+                              void *ws, size_t ws_bytes, holo_stream stream)
 {
     HOLO_TRY(check_n(n));
     HOLO_CHECK_ARG(n_frames >= 1 && n_sub >= 1, "n_frames and n_sub must be >= 1 (got %d, %d)", n_frames, n_sub);
@@ -722,9 +759,9 @@ extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_
     HOLO_TRY(fft::twiddles(&tw));
     cudaStream_t s = (cudaStream_t)stream;
     const float2 *l = (const float2 *)lut;
-#define HOLO_OSPR_CASE(NN)                                                                         \
-    case NN:                                                                                       \
-        return ospr_run<NN>(tw, target, n_frames, n_sub, l, n_lut, phase_offset, sf_begin, sf_end,     \
+#define HOLO_OSPR_CASE(NN)                                                                                 \
+    case NN:                                                                                               \
+        return ospr_run<NN>(tw, target, n_frames, n_sub, l, n_lut, prng, seed, phase_offset, sf_begin, sf_end, \
                             holo_bits, intensity, mse, omega, ws, s);
     switch (n) {
         HOLO_OSPR_CASE(16)
@@ -739,6 +776,25 @@ extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_
         return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }
 #undef HOLO_OSPR_CASE
+}
+
+extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
+                                          const holo_c64 *lut, uint64_t n_lut, uint64_t phase_offset,
+                                          int32_t sf_begin, int32_t sf_end, uint8_t *holo_bits,
+                                          float *intensity, double *mse, holo_region omega, void *ws,
+                                          size_t ws_bytes, holo_stream stream)
+{
+    return ospr_entry(target, n, n_frames, n_sub, lut, n_lut, false, 0, phase_offset, sf_begin, sf_end, holo_bits,
+                      intensity, mse, omega, ws, ws_bytes, stream);
+}
+
+extern "C" holo_status holo_ospr_generate_prng(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
+                                               uint64_t seed, uint64_t phase_offset, int32_t sf_begin,
+                                               int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse,
+                                               holo_region omega, void *ws, size_t ws_bytes, holo_stream stream)
+{
+    return ospr_entry(target, n, n_frames, n_sub, nullptr, 0, true, seed, phase_offset, sf_begin, sf_end, holo_bits,
+                      intensity, mse, omega, ws, ws_bytes, stream);
 }
 
 extern "C" holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, int32_t n,

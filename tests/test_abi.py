@@ -136,7 +136,7 @@ def test_plan_queries(L):
     assert L.holo_ospr_chunk_pairs(1024, 24) == 12          # C3: one L2-sized chunk of 12 pairs
     assert L.holo_ospr_chunk_pairs(64, 7) == 4
     assert L.holo_ospr_chunk_pairs(100, 7) == 0 and L.holo_ospr_chunk_pairs(64, 0) == 0
-    assert L.holo_gs_group_frames(1024, 64) == 16
+    assert L.holo_gs_group_frames(1024, 64) == 64
     assert L.holo_gs_group_frames(64, 3) == 3
     assert L.holo_gs_group_frames(64, 0) == 0
     assert L.holo_ospr_finalize_workspace_size() >= 592 * 5 * 8 + 4

@@ -257,3 +257,38 @@ def test_ospr_graph_replay_bit_identical():
     torch.cuda.synchronize()
     assert torch.equal(out.bits, eager.bits) and torch.equal(out.intensity, eager.intensity)
     assert torch.equal(out.mse, eager.mse)
+
+
+@pytest.mark.parametrize("n,S,offset", [(64, 8, 0), (128, 5, 12345), (256, 6, (1 << 33) + 7)])
+def test_ospr_prng_source_equals_full_length_lut(n, S, offset):
+    """phases drawn on the fly (SplitMix64 + R-5 in pass A) give
+    bit-identical holograms, intensity and MSE to a pool from the same seed that is longer
+    than every draw index -- here the pool covers [0, offset + S N^2)."""
+    T = cuda_target(blobs_target(7, n, 6, 4.0, 10.0, Region.upper_half(n)))
+    seed = 2004
+    ref = None
+    if offset + S * n * n < (1 << 31):
+        ref = hb.ospr_generate(T, S, hb.lut_generate(seed, offset + S * n * n), phase_offset=offset)
+    got = hb.ospr_generate(T, S, prng_seed=seed, phase_offset=offset)
+    if ref is not None:
+        assert torch.equal(got.bits, ref.bits) and torch.equal(got.intensity, ref.intensity)
+        assert torch.equal(got.mse, ref.mse)
+    else:
+        # beyond any pool: the oracle's own PRNG source (apply_phase_prng) + fp64 IDFT, P-3 band
+        Tn = to_np(T)
+        bits = to_np(got.bits)[0]
+        for s in range(S):
+            h_re = oracle.fft2(oracle.apply_phase_prng(Tn, seed, offset + s * n * n), True).real
+            check_bits(bits[s], h_re, n)
+
+
+def test_ospr_prng_c3_matches_full_length_pool():
+    """C3 size, full N_SF = 24: on-the-fly phases == the 25,165,824-entry pool (BASELINE
+    configs[2]'s full-frame PRNG baseline)."""
+    w = WORKLOADS["C3"]
+    T = cuda_target(target_for(w))
+    lut = hb.lut_generate(LUT_SEED, w.n * w.n * w.n_sub)
+    ref = hb.ospr_generate(T, w.n_sub, lut)
+    got = hb.ospr_generate(T, w.n_sub, prng_seed=LUT_SEED)
+    assert torch.equal(got.bits, ref.bits) and torch.equal(got.intensity, ref.intensity)
+    assert torch.equal(got.mse, ref.mse)
