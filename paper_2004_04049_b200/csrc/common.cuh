@@ -161,14 +161,15 @@ __device__ __forceinline__ float2 cmul_cs(float2 a, float c, float s)
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
-// 1/sqrt(x) for x > 0: hardware estimate + one Newton step (about 1 ulp; a few
-// branch-free instructions instead of the IEEE sqrt + divide sequences, whose code
-// size per unrolled element overflows the instruction cache).
-__device__ __forceinline__ float rsqrt_nr(float x)
+// 1/sqrt(x) for normal x > 0: one SFU instruction (rsqrt.approx.ftz, relative error
+// below 2^-22).  Callers treat x < kFltMin (zero, or a denormal the SFU flushes) as zero.
+__device__ __forceinline__ float rsqrt_sfu(float x)
 {
-    const float r = rsqrtf(x);
-    return __fmul_rn(r, __fmaf_rn(__fmul_rn(-0.5f, x), __fmul_rn(r, r), 1.5f));
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
+constexpr float kFltMin = 1.17549435082228750797e-38f;   // smallest normal fp32
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
 // ---- cyclic LUT index (step a1) ----------------------------------------------------------

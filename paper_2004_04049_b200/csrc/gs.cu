@@ -103,7 +103,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
 // ---- column pass: IFFT -> constraint -> FFT (TMA-fed pipeline) ----------------------------------
 template <int N, bool QUANT>
 struct GsColBody {
-    static constexpr int kStages = 1;   // measured best column-pipeline variant for this body
+    static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     struct Args {
         const float2 *tw;
         float2 *buf;          // the group's state (updated in place)
@@ -138,13 +138,9 @@ struct GsColBody {
                 float2 o;
                 int j = 0;
                 if constexpr (!QUANT) {
-                    const float m2 = hk.x * hk.x + hk.y * hk.y;
-                    if (m2 == 0.0f) {
-                        o = make_float2(1.0f, 0.0f);           // R-16: H = 0 -> +1
-                    } else {
-                        const float rr = rsqrt_nr(m2);
-                        o = make_float2(hk.x * rr, hk.y * rr);
-                    }
+                    const float m2 = __fmaf_rn(hk.x, hk.x, __fmul_rn(hk.y, hk.y));
+                    o = m2 < kFltMin ? make_float2(1.0f, 0.0f)               // R-16: H = 0 -> +1
+                                     : f2::mul(hk, f2::bc(rsqrt_sfu(m2)));   // H / |H|
                 } else {
                     float th = atan2f(hk.y, hk.x);
                     if (th < 0.0f)
@@ -255,7 +251,8 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                 // explicit rounding: identical arithmetic in every instantiation (fused == step)
                 const float m2 = __fmaf_rn(X.x, X.x, __fmul_rn(X.y, X.y));
                 const float I = __fmul_rn(m2, inv_n * inv_n);
-                const float rr = m2 > 0.0f ? rsqrt_nr(m2) : 0.0f;
+                const bool nz = m2 >= kFltMin;
+                const float rr = nz ? rsqrt_sfu(m2) : 0.0f;
                 const float amp = __fmul_rn(__fmul_rn(m2, rr), inv_n);   // |R'_k|
                 const float tt = tv[r];
                 const float d = __fsub_rn(amp, tt);
@@ -270,7 +267,7 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                         inten[rofs + x] = I;
                 }
                 if (MODE != GS_LAST)
-                    v[r] = m2 > 0.0f ? f2::mul(X, f2::bc(__fmul_rn(tt, rr)))   // R = T X / |X|
+                    v[r] = nz ? f2::mul(X, f2::bc(__fmul_rn(tt, rr)))          // R = T X / |X|
                                      : make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
             }
             sums[0] = (double)sI;
