@@ -170,6 +170,35 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
                 const Base b1 = PR::row(ps, bb, y), b2 = PR::row(ps, bb, ym);
                 const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
                 constexpr int M = N < 32 ? 1 : N / 32;
+                if constexpr (LMODE == LUT_WRAP && N >= 64) {
+                    // No index of the four LUT rows wraps (the usual case; always for L a
+                    // multiple of N with an aligned offset): every load of the row pair is a
+                    // fixed offset from a per-lane base pointer, no per-pixel index arithmetic.
+                    const uint32_t lim = ps.ix.L - (uint32_t)N;
+                    if (a1 <= lim && a2 <= lim && b1 <= lim && b2 <= lim) {
+                        const float2 *LA1 = ps.lut + a1 + lane, *LB1 = ps.lut + b1 + lane;
+                        const float2 *LA2 = ps.lut + a2 + (N - lane), *LB2 = ps.lut + b2 + (N - lane);
+                        const float *T1l = T1 + lane, *T2l = T2 + (N - lane);
+                        float2 *S0 = s0 + lane, *S1 = s1 + (N - lane);
+                        {   // m = 0: the mirror of x = 0 is 0, not N
+                            const int xm = (N - lane) & (N - 1);
+                            const float t1 = T1l[0], t2 = T2[xm];
+                            const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[0], ps.lut[a2 + xm], LB1[0],
+                                                   ps.lut[b2 + xm]);
+                            S0[0] = z.z1;
+                            s1[xm] = z.z2;
+                        }
+#pragma unroll 16
+                        for (int m = 1; m < M; ++m) {
+                            const float t1 = T1l[32 * m], t2 = T2l[-32 * m];
+                            const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[32 * m], LA2[-32 * m], LB1[32 * m],
+                                                   LB2[-32 * m]);
+                            S0[32 * m] = z.z1;
+                            S1[-32 * m] = z.z2;
+                        }
+                        continue;
+                    }
+                }
 #pragma unroll (LMODE == LUT_PRNG ? 2 : 16)
                 for (int m = 0; m < M; ++m) {
                     const int x = lane + 32 * m;
