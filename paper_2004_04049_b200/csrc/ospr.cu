@@ -40,7 +40,7 @@ static holo_status flat_lut(const float2 **p)
     return HOLO_OK;
 }
 
-constexpr int kFinBlocks = 1184;  // finalize CTAs per frame (fixed => deterministic sums)
+constexpr int kFinBlocks = 592;   // finalize CTAs per frame (fixed => deterministic sums; 4 per SM)
 constexpr int kFinThreads = 256;
 constexpr size_t kFinWsBytes = (size_t)kFinBlocks * 5 * sizeof(double) + 256;   // partial sums + ticket
 
@@ -540,7 +540,7 @@ __device__ __forceinline__ double mse_from_sums(const double *o, double inv_coun
 template <int N>
 __global__ void __launch_bounds__(kFinThreads)
 ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T, int symmetrise, float scale,
-                     float *out, holo_region om, double *__restrict__ parts, unsigned *counter, double inv_count,
+                     float *__restrict__ out, holo_region om, double *__restrict__ parts, unsigned *counter, double inv_count,
                      double *__restrict__ mse, int fb, const uint8_t *__restrict__ bt, uint8_t *__restrict__ bits)
 {
     HOLO_PDL_ENTRY();
@@ -551,7 +551,7 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
     }
     constexpr int P = N * N, LOG = fft::ilog2(N);
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
+#pragma unroll 8
     for (int k = blockIdx.x * kFinThreads + threadIdx.x; k < P; k += fb * kFinThreads) {
         const int y = k >> LOG, x = k & (N - 1);
         float I;
@@ -651,7 +651,7 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
 
 static int fin_grid(int n)
 {
-    const int want = (n * n + 4 * kFinThreads - 1) / (4 * kFinThreads);   // >= 4 pixels per thread
+    const int want = (n * n + 7 * kFinThreads - 1) / (7 * kFinThreads);   // about 7 pixels per thread
     return want < kFinBlocks ? want : kFinBlocks;
 }
 
