@@ -253,6 +253,122 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
     }
 }
 
+// Pass A for N >= 1024 (one row per warp item): a unit {y, N - y} is shared by a PAIR of warps.
+// Each warp builds the Z pixel pairs of one half of the columns (both rows), the pair meets at
+// a named barrier, then each warp row-IFFTs one of the two rows in place.  One row slot per warp
+// (instead of two) and pool twiddles (instead of registers) let half again as many warps reside
+// per SM, to hide the producer's L2 latency.
+template <int N>
+struct RowA2 {
+    using P = fft::Plan<N>;
+    static_assert(32 / P::T == 1, "one row per warp item");
+    static constexpr int WPC = 4, UPC = WPC / 2;                 // warps, units per CTA
+    static constexpr uint32_t SLOT = ((uint32_t)P::SMEM * 8 + 127) / 128 * 128;   // one row
+    static constexpr size_t SMEM = (size_t)WPC * SLOT;
+    static constexpr int UNITS_PER_PAIR = N / 2;
+};
+
+template <int N, int LMODE>
+__global__ void __launch_bounds__(RowA2<N>::WPC * 32)
+ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
+                    int npairs, int last_pair_has_b, float2 *__restrict__ buf)
+{
+    HOLO_PDL_ENTRY();
+    using P = fft::Plan<N>;
+    using RA = RowA2<N>;
+    using PR = PhaseRows<N, LMODE>;
+    using Base = typename PR::Base;
+    constexpr int R1 = P::R1, E = P::E, M = N / 32, MH = M / 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = lane;
+    const int up = warp >> 1, h = warp & 1;                      // unit slot in the CTA, half
+    float2 *s0 = reinterpret_cast<float2 *>(smem_raw + (size_t)(2 * up) * RA::SLOT);
+    float2 *s1 = reinterpret_cast<float2 *>(smem_raw + (size_t)(2 * up + 1) * RA::SLOT);
+    const float2 *twp = tw;
+    const int nunits = npairs * RA::UNITS_PER_PAIR;
+    #pragma unroll 1
+    for (int u = blockIdx.x * RA::UPC + up; u < nunits; u += gridDim.x * RA::UPC) {
+        const int pair = u / RA::UNITS_PER_PAIR, k = u % RA::UNITS_PER_PAIR;
+        const bool has_b = (pair < npairs - 1) || last_pair_has_b;
+        const Base ba = PR::subframe(ps, sf_first + 2 * (uint64_t)pair);
+        const Base bb = PR::subframe(ps, sf_first + 2 * (uint64_t)pair + 1);
+        const float bsc = has_b ? 1.0f : 0.0f;   // an absent sub-frame b contributes R_b = 0
+        const int y = k, ym = k > 0 ? N - k : N / 2;
+        if (k > 0) {   // pixel pairs (y, x) <-> (ym, N - x), this warp: x in [h N/2, (h+1) N/2)
+            const int x0 = h * (N / 2);
+            const Base a1 = PR::row(ps, ba, y), a2 = PR::row(ps, ba, ym);
+            const Base b1 = PR::row(ps, bb, y), b2 = PR::row(ps, bb, ym);
+            const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
+            bool fast = false;
+            if constexpr (LMODE == LUT_WRAP) {
+                const uint32_t lim = ps.ix.L - (uint32_t)N;
+                fast = a1 <= lim && a2 <= lim && b1 <= lim && b2 <= lim;
+            }
+            if (fast) {   // no LUT row wraps: fixed offsets from per-lane base pointers
+                const int xl = x0 + lane;
+                const float2 *LA1 = ps.lut + (uint32_t)a1 + xl, *LB1 = ps.lut + (uint32_t)b1 + xl;
+                const float2 *LA2 = ps.lut + (uint32_t)a2 + (N - xl), *LB2 = ps.lut + (uint32_t)b2 + (N - xl);
+                const float *T1l = T1 + xl, *T2l = T2 + (N - xl);
+                float2 *S0 = s0 + xl, *S1 = s1 + (N - xl);
+                {   // m = 0: the mirror of x = 0 is 0, not N
+                    const int xm = (N - xl) & (N - 1);
+                    const float t1 = T1l[0], t2 = T2[xm];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[0], ps.lut[(uint32_t)a2 + xm], LB1[0],
+                                           ps.lut[(uint32_t)b2 + xm]);
+                    S0[0] = z.z1;
+                    s1[xm] = z.z2;
+                }
+#pragma unroll
+                for (int m = 1; m < MH; ++m) {
+                    const float t1 = T1l[32 * m], t2 = T2l[-32 * m];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[32 * m], LA2[-32 * m], LB1[32 * m],
+                                           LB2[-32 * m]);
+                    S0[32 * m] = z.z1;
+                    S1[-32 * m] = z.z2;
+                }
+            } else {
+#pragma unroll (LMODE == LUT_PRNG ? 2 : 8)
+                for (int m = 0; m < MH; ++m) {
+                    const int x = x0 + lane + 32 * m, xm = (N - x) & (N - 1);
+                    const float t1 = T1[x], t2 = T2[xm];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a2, xm),
+                                           PR::at(ps, b1, x), PR::at(ps, b2, xm));
+                    s0[x] = z.z1;
+                    s1[xm] = z.z2;
+                }
+            }
+        } else {       // unit 0: rows 0 and N/2, each its own mirror; this warp builds row h
+            const int yy = h ? N / 2 : 0;
+            float2 *d = h ? s1 : s0;
+            const Base a1 = PR::row(ps, ba, yy), b1 = PR::row(ps, bb, yy);
+            const float *T1 = T + (size_t)yy * N;
+            for (int x = lane; x <= N / 2; x += 32) {
+                const int xm = (N - x) & (N - 1);
+                const float t1 = T1[x], t2 = T1[xm];
+                const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a1, xm),
+                                       PR::at(ps, b1, x), PR::at(ps, b1, xm));
+                d[x] = z.z1;
+                d[xm] = z.z2;
+            }
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + up) : "memory");   // both halves of Z are built
+        // row IFFT of row (h ? ym : y) in place: F^-1{x} = conj(F{conj(x)})
+        float2 *sg = h ? s1 : s0;
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            v[m] = sg[t + R1 * m];
+            v[m].y = -v[m].y;
+        }
+        fft::fft2pass<N, false, 1, true>(v, sg, t, twp);
+        float2 *o = buf + ((size_t)pair * N + (h ? ym : y)) * N;
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            o[t + R1 * m] = make_float2(v[m].x, -v[m].y);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + up) : "memory");   // both rows read before reuse
+    }
+}
+
 // ---- pass B: column IFFT -> a4 sign + pack -> column FFT (TMA-fed pipeline) ------------------
 // 8x8 bit-matrix transpose (bit 8i + j <-> bit 8j + i), three masked swap stages.
 __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
@@ -704,13 +820,24 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             {
                 using RA = RowA<N>;
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG>
-                          : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
-                          : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2>
-                                                   : ospr_rows_a_kernel<N, LUT_GENERAL>;
-                const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
-                HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, ps, sf_first,
-                                np, last_has_b, w.buf));
+                if constexpr (N >= 1024) {
+                    using RA2 = RowA2<N>;
+                    auto kern = prng                     ? ospr_rows_a2_kernel<N, LUT_PRNG>
+                              : ps.ix.mode == LUT_WRAP ? ospr_rows_a2_kernel<N, LUT_WRAP>
+                              : ps.ix.mode == LUT_POW2 ? ospr_rows_a2_kernel<N, LUT_POW2>
+                                                       : ospr_rows_a2_kernel<N, LUT_GENERAL>;
+                    const int grid = pipe_grid(kern, RA2::WPC * 32, RA2::SMEM, np * RA2::UNITS_PER_PAIR, RA2::UPC);
+                    HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA2::WPC * 32), RA2::SMEM, s, tw, Tf, ps,
+                                    sf_first, np, last_has_b, w.buf));
+                } else {
+                    auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG>
+                              : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
+                              : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2>
+                                                       : ospr_rows_a_kernel<N, LUT_GENERAL>;
+                    const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
+                    HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, ps,
+                                    sf_first, np, last_has_b, w.buf));
+                }
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
