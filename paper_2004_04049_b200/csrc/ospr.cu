@@ -414,17 +414,24 @@ struct OsprColBody {
             }
             fft.template run<false, W>(v, sm, t);
             if (h == 0) {                                        // v = conj(H) (x N): Re H = v.x, Im H = -v.y
+                // u = (Re H, Im H) + 0 (one FADD2): -0.0 becomes +0.0, so u's sign bit is set iff
+                // the value is < 0, and h' = +-1 is that sign bit on 1.0f (R-7: Re H >= 0 -> +1)
 #pragma unroll
                 for (int r = 0; r < E; ++r) {
-                    wa |= (Word)(v[r].x >= 0.0f) << r;           // -0.0 -> +1 (R-7)
-                    wb |= (Word)(v[r].y <= 0.0f) << r;           // Im H = -v.y >= 0
+                    const float2 u = f2::add(conjf2(v[r]), make_float2(0.0f, 0.0f));
+                    const uint32_t ua = __float_as_uint(u.x), ub = __float_as_uint(u.y);
+                    wa |= (Word)((~ua) >> 31) << r;
+                    wb |= (Word)((~ub) >> 31) << r;
+                    v[r] = make_float2(__uint_as_float((ua & 0x80000000u) | 0x3f800000u),
+                                       __uint_as_float((ub & 0x80000000u) | 0x3f800000u));
+                }
+                if (!has_b) {                                    // unpaired tail: h'_b = 0
+#pragma unroll
+                    for (int r = 0; r < E; ++r)
+                        v[r].y = 0.0f;
                 }
                 sw[t * W + c] = wa;                              // read back after the next FFT's barriers
                 sw[(R1 + t) * W + c] = wb;
-#pragma unroll
-                for (int r = 0; r < E; ++r)
-                    v[r] = make_float2(((wa >> r) & 1) ? 1.0f : -1.0f,
-                                       has_b ? (((wb >> r) & 1) ? 1.0f : -1.0f) : 0.0f);
             }
         }
         // (the pipeline stores v, the column FFT of h')
