@@ -323,7 +323,7 @@ def run_gpu(args):
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Gaussian-blob targets, holo_synth; stands in for USC-SIPI images)",
         "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step (a0 LUT build + "
                                "a1-a7 incl. MSE); BASELINE configs[2]",
@@ -503,7 +503,7 @@ def run_reference(args):
     v = w3.n_sub * steps / dt
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step; BASELINE configs[2]",
                    "lut_len": args.lut},
