@@ -170,7 +170,6 @@ __device__ __forceinline__ float rsqrt_sfu(float x)
     return r;
 }
 constexpr float kFltMin = 1.17549435082228750797e-38f;   // smallest normal fp32
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
 // ---- cyclic LUT index (step a1) ----------------------------------------------------------
 // idx = (rowbase + x) mod L for rowbase < L, x < N, evaluated per pixel without a

@@ -189,7 +189,7 @@ struct Plan {
 // Pool size: sum over N = 16..2048 of N = 4080 entries.  Built once per device by
 // holo::fft::twiddles() (host libm in double, rounded to fp32) in library-owned
 // device memory; kernels receive the pool pointer as an argument.
-constexpr int kTwPool = 8448;   // 4080 two-pass entries + three-pass tables from offset 4096
+constexpr int kTwPool = 4096;   // 4080 two-pass entries (N = 16 .. 2048)
 holo_status twiddles(const float2 **pool);
 
 __device__ __forceinline__ int pad_index(int i, int r1) { return i + i / r1; }
@@ -318,88 +318,6 @@ __device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, in
     fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwRegs<N, REG>{tw});
 }
 
-// ---- three-pass variant (E = 16 values per thread) ------------------------------------------
-// N = RA * RB * RC with RA = 16; T = N/16 threads per transform.  Used by the column
-// pipelines for N >= 512, where two passes would need E = 32..64 registers' worth of
-// values per thread and so too few warps per SM.  Pass p (radix R, stride Ns) runs
-// butterflies j = t + T*q on slots q + (E/R)*r and writes index
-// (j/Ns)*Ns*R + j%Ns + r*Ns (Stockham); every pass reads the natural map t + T*m.
-// Twiddle tables in the pool: pass B  W_{RA*RB}^{r*k} at TWB + r*RA + k (k < RA),
-//                             pass C  W_N^{r*k}       at TWC + r*(N/RC) + k.
-template <int N>
-struct Plan3 {
-    static_assert(N == 512 || N == 1024 || N == 2048, "three-pass plans cover N = 512..2048");
-    static constexpr int E = 16, RA = 16, RB = (N == 512) ? 8 : 16, RC = N / (RA * RB);
-    static constexpr int T = N / E, BA = E / RA, BB = E / RB, BC = E / RC;
-    static constexpr int SMEM = N + N / 16;       // padded exchange buffer (pad every 16)
-    static constexpr int TWB = 4096 + (N == 512 ? 0 : (N == 1024 ? 640 : 1920));
-    static constexpr int TWC = TWB + RA * RB;
-};
-
-template <int N, bool INV, int IL>
-__device__ __forceinline__ void fft3pass(float2 (&v)[16], float2 *sm, int t, const float2 *__restrict__ twp)
-{
-    using P = Plan3<N>;
-    constexpr int E = P::E, T = P::T, RA = P::RA, RB = P::RB, RC = P::RC;
-    constexpr int BA = P::BA, BB = P::BB, BC = P::BC;
-    auto at = [&](int i) -> float2 & { return sm[(i + i / 16) * IL]; };
-    // pass A (Ns = 1)
-#pragma unroll
-    for (int q = 0; q < BA; ++q)
-        Dft<RA, BA, INV>::run(v + q);
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < BA; ++q)
-#pragma unroll
-        for (int r = 0; r < RA; ++r)
-            at((t + T * q) * RA + r) = v[q + BA * r];
-    __syncthreads();
-    // pass B (Ns = RA)
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = at(t + T * m);
-    {
-        const float2 *twb = twp + P::TWB + (t % RA);
-#pragma unroll
-        for (int q = 0; q < BB; ++q)
-#pragma unroll
-            for (int r = 1; r < RB; ++r) {
-                float2 w = ldg_nocse(twb + r * RA);
-                if (INV)
-                    w.y = -w.y;
-                v[q + BB * r] = cmul(v[q + BB * r], w);
-            }
-    }
-#pragma unroll
-    for (int q = 0; q < BB; ++q)
-        Dft<RB, BB, INV>::run(v + q);
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < BB; ++q)
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-            const int j = t + T * q;
-            at((j / RA) * RA * RB + (j % RA) + r * RA) = v[q + BB * r];
-        }
-    __syncthreads();
-    // pass C (Ns = RA*RB)
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = at(t + T * m);
-#pragma unroll
-    for (int q = 0; q < BC; ++q)
-#pragma unroll
-        for (int r = 1; r < RC; ++r) {
-            float2 w = ldg_nocse(twp + P::TWC + r * (N / RC) + t + T * q);
-            if (INV)
-                w.y = -w.y;
-            v[q + BC * r] = cmul(v[q + BC * r], w);
-        }
-#pragma unroll
-    for (int q = 0; q < BC; ++q)
-        Dft<RC, BC, INV>::run(v + q);
-}
-
 // FFT policies for the column pipeline: element m of thread t is row t + T*m.
 template <int N, bool REG>
 struct ColFft2 {
@@ -414,18 +332,6 @@ struct ColFft2 {
     }
 };
 
-template <int N>
-struct ColFft3 {
-    using P = Plan3<N>;
-    static constexpr int E = P::E, T = P::T, SMEM = P::SMEM;
-    const float2 *twp;
-    __device__ __forceinline__ void init(const float2 *p, int) { twp = p; }
-    template <bool INV, int IL>
-    __device__ __forceinline__ void run(float2 (&v)[E], float2 *sm, int t) const
-    {
-        fft3pass<N, INV, IL>(v, sm, t, twp);
-    }
-};
 
 } // namespace fft
 } // namespace holo

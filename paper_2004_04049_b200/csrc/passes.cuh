@@ -18,16 +18,6 @@
 
 namespace holo {
 
-template <int N>
-struct RowShape {
-    using P = fft::Plan<N>;
-    static constexpr int GPW = 32 / P::T;                                   // row groups per warp
-    static constexpr int WPC = (N * P::T / 32) < 4 ? (N * P::T / 32) : 4;   // warps per CTA (<= N rows)
-    static constexpr int RPC = WPC * GPW;                                   // rows per CTA
-    static constexpr int THREADS = WPC * 32;
-    static constexpr size_t SMEM = (size_t)RPC * P::SMEM * sizeof(float2);
-};
-
 // ---- row pipeline ---------------------------------------------------------------------------
 // Warp-persistent, per-warp double-buffered: a work item is GPW = 32/T consecutive rows
 // (always 256*E contiguous bytes), fetched by one cp.async.bulk (1D TMA) into the warp's
@@ -151,9 +141,9 @@ holo_status launch_rows_fft(KernelId id, const float2 *tw, const float2 *in, flo
 }
 
 // ---- column pipeline -------------------------------------------------------------------------
-// FFT policy per size: the two-pass transform.  (The three-pass E = 16 policy
-// fft::ColFft3 doubles the warps per tile but measured slower on B200 at N = 1024:
-// its extra shared-memory exchange outweighs the occupancy gain.)
+// FFT policy per size: the two-pass transform.  (A three-pass E = 16 policy doubles the
+// warps per tile but measured 75 vs 52 us for the OSPR column pass at N = 1024: its extra
+// shared-memory exchange outweighs the occupancy gain; removed.)
 template <int N, bool REG>
 struct ColFftFor {
     using type = fft::ColFft2<N, REG>;

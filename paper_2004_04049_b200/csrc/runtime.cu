@@ -155,23 +155,6 @@ holo_status twiddles(const float2 **pool)
                 host[off + r * r1 + t] = make_float2((float)std::cos(a), (float)std::sin(a));
             }
     }
-    // three-pass tables (fft.cuh Plan3): N = 512 (16.8.4), 1024 (16.16.4), 2048 (16.16.8)
-    {
-        const int ns[3] = {512, 1024, 2048}, rbs[3] = {8, 16, 16}, offs[3] = {4096, 4096 + 640, 4096 + 1920};
-        for (int i = 0; i < 3; ++i) {
-            const int n = ns[i], ra = 16, rb = rbs[i], rc = n / (ra * rb), twb = offs[i], twc = twb + ra * rb;
-            for (int r = 0; r < rb; ++r)
-                for (int k = 0; k < ra; ++k) {
-                    double a = -2.0 * 3.14159265358979323846 * (double)((r * k) % (ra * rb)) / (double)(ra * rb);
-                    host[twb + r * ra + k] = make_float2((float)std::cos(a), (float)std::sin(a));
-                }
-            for (int r = 0; r < rc; ++r)
-                for (int k = 0; k < n / rc; ++k) {
-                    double a = -2.0 * 3.14159265358979323846 * (double)(((long long)r * k) % n) / (double)n;
-                    host[twc + r * (n / rc) + k] = make_float2((float)std::cos(a), (float)std::sin(a));
-                }
-        }
-    }
     float2 *d = nullptr;
     e = cudaMalloc(&d, sizeof(float2) * kTwPool);
     if (e != cudaSuccess)
