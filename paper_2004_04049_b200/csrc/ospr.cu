@@ -546,9 +546,11 @@ struct RowC {
 template <int N>
 __global__ void __launch_bounds__(64)
 ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
-                   float *__restrict__ acc, int accumulate)
+                   float *__restrict__ acc, int accumulate, unsigned *ticket)
 {
     HOLO_PDL_ENTRY();
+    if (ticket != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+        *ticket = 0u;                    // the finalize ticket, reset ahead of the finalize kernel
     using P = fft::Plan<N>;
     using RC = RowC<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RC::GPW, NGRP = RC::NGRP;
@@ -772,6 +774,9 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
 }
 
 
+// The completion ticket of the finalize kernel, after its per-CTA partial-sum slots.
+static unsigned *finalize_ticket(double *parts) { return reinterpret_cast<unsigned *>(parts + (size_t)kFinBlocks * 5); }
+
 static int fin_grid(int n)
 {
     const int want = (n * n + 7 * kFinThreads - 1) / (7 * kFinThreads);   // about 7 pixels per thread
@@ -781,12 +786,13 @@ static int fin_grid(int n)
 // Finalize one frame (and, if bits != NULL, transpose its nq sub-frames of sign bytes).
 template <int N>
 holo_status finalize_frame(const float *acc, const float *T, int symmetrise, float scale, float *out, holo_region om,
-                           double *parts, double *mse, const uint8_t *bt, uint8_t *bits, int nq, cudaStream_t s)
+                           double *parts, double *mse, const uint8_t *bt, uint8_t *bits, int nq, cudaStream_t s,
+                           bool ticket_zeroed = false)
 {
     const int fb = fin_grid(N);
-    unsigned *counter = reinterpret_cast<unsigned *>(parts + (size_t)kFinBlocks * 5);
+    unsigned *counter = finalize_ticket(parts);
     const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
-    if (mse) {
+    if (mse && !ticket_zeroed) {
         cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
         if (e != cudaSuccess)
             return cuda_status(e, "cudaMemsetAsync(finalize ticket)");
@@ -852,13 +858,13 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                 using RC = RowC<N>;
                 const int grid = pipe_grid(ospr_rows_c_kernel<N>, 64, RC::SMEM, RC::NGRP, 1);
                 HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(grid), dim3(64), RC::SMEM, s, tw,
-                                (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0));
+                                (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0, finalize_ticket(w.parts)));
             }
         }
         const float scale = full ? 0.5f / (float)n_sub : 0.5f;
         HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
                                    (full && mse) ? mse + f : nullptr, w.bt,
-                                   holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr, nsh, s));
+                                   holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr, nsh, s, true));
     }
     return HOLO_OK;
 }
