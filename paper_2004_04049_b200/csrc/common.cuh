@@ -74,8 +74,8 @@ holo_status launch(KernelId id, void (*kernel)(KArgs...), dim3 grid, dim3 block,
 {
     if (grid.x == 0 || grid.y == 0 || grid.z == 0)
         return HOLO_OK;
-    if (smem > 48 * 1024)
-        HOLO_TRY(ensure_smem((const void *)kernel, smem));
+    if (smem > 0)
+        HOLO_TRY(ensure_smem((const void *)kernel, smem));   // cached per kernel and device
     prof_before(id, s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;

@@ -240,9 +240,9 @@ struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
 
-// `after_exchange` runs once every value has been read back from the exchange buffer and
-// consumed (pass-2 twiddles applied), before the pass-2 DFT: the buffer may be refilled
-// from there on (row pipelines issue their next TMA load into it, WS = true only).
+// `after_exchange` runs once every value has been read back from the exchange buffer, before
+// the pass-2 DFT: a caller refilling the buffer by TMA from there on must first order those
+// reads before the async-proxy write (fence.proxy.async + __syncwarp; WS = true only).
 template <int N, bool INV, int IL, bool WS, class TwSrc, class Hook = NoHook>
 __device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *sm, int t, const TwSrc &tws,
                                               const Hook &after_exchange = Hook())

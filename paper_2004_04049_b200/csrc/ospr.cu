@@ -474,13 +474,13 @@ struct OsprColBody {
 // Tile-major sign bytes bt[q][ct][y] (ct < N/8, y < N) -> row-major packed holograms
 // out[q][y][ct] (R-8), one block of YB rows of sub-frame q per CTA, through shared memory;
 // 32-bit words on both global sides when N >= 32 (every thread's loads in flight at once).
-// Run by the extra CTAs of ospr_finalize_kernel (256 threads).
+// Run by extra CTAs of ospr_rows_c_kernel (64 threads) or ospr_finalize_kernel (256 threads).
 template <int N>
 struct BitsT {
     static constexpr int C = N / 8, YB = N < 32 ? N : 32, BLOCKS_PER_Q = N / YB;
 };
 
-template <int N>
+template <int N, int NT = 256>
 __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__ bt, uint8_t *__restrict__ out, int q,
                                                      int yblk)
 {
@@ -490,16 +490,16 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
     const uint8_t *src = bt + (size_t)q * C * N + y0;
     uint8_t *dst = out + ((size_t)q * N + y0) * C;
     if constexpr (N >= 32) {
-        constexpr int WPR = YB / 4, WORDS = C * WPR, PER = (WORDS + 255) / 256;   // words per ct row
+        constexpr int WPR = YB / 4, WORDS = C * WPR, PER = (WORDS + NT - 1) / NT;   // words per ct row
         uint32_t w[PER];
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
-            const int i = threadIdx.x + 256 * j;
+            const int i = threadIdx.x + NT * j;
             w[j] = i < WORDS ? __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(i / WPR) * N) + i % WPR) : 0u;
         }
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
-            const int i = threadIdx.x + 256 * j;
+            const int i = threadIdx.x + NT * j;
             if (i < WORDS)
                 *reinterpret_cast<uint32_t *>(&sm[i / WPR][4 * (i % WPR)]) = w[j];
         }
@@ -507,7 +507,7 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
         constexpr int OW = C / 4;   // output words per row
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
-            const int i = threadIdx.x + 256 * j;
+            const int i = threadIdx.x + NT * j;
             if (i < WORDS) {
                 const int y = i / OW, c4 = 4 * (i % OW);
                 const uint32_t v = (uint32_t)sm[c4][y] | ((uint32_t)sm[c4 + 1][y] << 8) |
@@ -546,11 +546,18 @@ struct RowC {
 template <int N>
 __global__ void __launch_bounds__(64)
 ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
-                   float *__restrict__ acc, int accumulate, unsigned *ticket)
+                   float *__restrict__ acc, int accumulate, unsigned *ticket, int nbt, const uint8_t *__restrict__ bt,
+                   uint8_t *__restrict__ bits)
 {
     HOLO_PDL_ENTRY();
-    if (ticket != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    if ((int)blockIdx.x < nbt) {         // the frame's sign-byte transposes (last chunk), scheduled first
+        const int j = (int)blockIdx.x;
+        bits_transpose_block<N, 64>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
+        return;
+    }
+    if (ticket != nullptr && blockIdx.x == nbt && threadIdx.x == 0)
         *ticket = 0u;                    // the finalize ticket, reset ahead of the finalize kernel
+    const int cta = (int)blockIdx.x - nbt, nctas = (int)gridDim.x - nbt;
     using P = fft::Plan<N>;
     using RC = RowC<N>;
     constexpr int R1 = P::R1, E = P::E, GPW = RC::GPW, NGRP = RC::NGRP;
@@ -567,14 +574,14 @@ ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf
         tma::fence_mbar_init();
     }
     __syncwarp();
-    int grp = blockIdx.x;
+    int grp = cta;
     if (lane == 0 && grp < NGRP && p0 < p1) {
         tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
         tma::load_1d(sl, src(grp, p0), RC::IN_BYTES, bar);
     }
     uint32_t k = 0;
     #pragma unroll 1
-    for (; grp < NGRP; grp += gridDim.x) {
+    for (; grp < NGRP; grp += nctas) {
         float a[E];
 #pragma unroll
         for (int r = 0; r < E; ++r)
@@ -586,10 +593,13 @@ ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf
 #pragma unroll
             for (int m = 0; m < E; ++m)
                 v[m] = sl[g * N + t + R1 * m];
-            const bool more = (p + 1 < p1) || (grp + (int)gridDim.x < NGRP);
-            const float2 *nx = (p + 1 < p1) ? src(grp, p + 1) : src(grp + gridDim.x, p0);
+            const bool more = (p + 1 < p1) || (grp + nctas < NGRP);
+            const float2 *nx = (p + 1 < p1) ? src(grp, p + 1) : src(grp + nctas, p0);
             fft::fft2pass_hook<N, false, 1, true>(v, sl + g * P::SMEM, t, tw, [&] {
-                __syncwarp();                            // every lane has consumed the exchange
+                // WAR across proxies: every lane's exchange reads are performed (proxy fence)
+                // before lane 0's TMA write into the same slot is issued
+                tma::fence_proxy_async_smem();
+                __syncwarp();
                 if (lane == 0 && more) {
                     tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
                     tma::load_1d(sl, nx, RC::IN_BYTES, bar);
@@ -856,15 +866,17 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
             {
                 using RC = RowC<N>;
+                const bool last = c0 + np >= npairs_total;
+                const int nbt = (last && holo_bits) ? nsh * BitsT<N>::BLOCKS_PER_Q : 0;
                 const int grid = pipe_grid(ospr_rows_c_kernel<N>, 64, RC::SMEM, RC::NGRP, 1);
-                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(grid), dim3(64), RC::SMEM, s, tw,
-                                (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0, finalize_ticket(w.parts)));
+                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(nbt + grid), dim3(64), RC::SMEM, s, tw,
+                                (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0, finalize_ticket(w.parts), nbt,
+                                (const uint8_t *)w.bt, holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr));
             }
         }
         const float scale = full ? 0.5f / (float)n_sub : 0.5f;
         HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
-                                   (full && mse) ? mse + f : nullptr, w.bt,
-                                   holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr, nsh, s, true));
+                                   (full && mse) ? mse + f : nullptr, nullptr, nullptr, 0, s, true));
     }
     return HOLO_OK;
 }

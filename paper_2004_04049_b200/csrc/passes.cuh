@@ -120,7 +120,7 @@ inline int pipe_grid(K kernel, int threads, size_t smem, int nitems, int wpc)
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (smem > 48 * 1024)
+    if (smem > 0)
         ensure_smem((const void *)kernel, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (per_sm < 1)

@@ -121,7 +121,19 @@ holo_status ensure_smem(const void *fn, size_t smem)
     auto key = std::make_pair(dev, fn);
     if (g_smem_done.count(key))
         return HOLO_OK;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // opt in to the largest dynamic size this kernel can have next to its static shared memory
+    // (static + dynamic above 48 KB needs the opt-in even when the dynamic part alone is below)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaFuncGetAttributes");
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int dyn = optin - (int)fa.sharedSizeBytes;
+    if ((size_t)dyn < smem)
+        return set_error(HOLO_ERR_CUDA, "kernel needs %zu + %zu bytes of shared memory > %d", smem, fa.sharedSizeBytes,
+                         optin);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     if (e != cudaSuccess)
         return cuda_status(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
     g_smem_done.insert(key);

@@ -318,3 +318,17 @@ def test_f1_lut_sweep_shape_and_oracle_point():
     j = keys.index(("lut", 13))
     _, _, mse_ref = oracle.ospr(T, ls.N_SF, oracle.lut_build(7000, 13), 0, Region.upper_half(n).as_tuple())
     assert np.all(np.abs(mse[j, 0] - mse_ref) <= 1e-4 * np.abs(mse_ref))
+
+
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_ospr_repeat_bit_identical_multichunk(n, monkeypatch):
+    """Repeated calls are bit-identical at the large sizes too, with several chunks (the pass-C
+    accumulator round trip and its TMA slot refills): guards the cross-proxy WAR ordering of
+    the single-slot row pipeline (a missing proxy fence made N = 2048 intensities vary)."""
+    monkeypatch.setenv("HOLO_OSPR_CHUNK_BYTES", str(2 * n * n * 8))      # 2 pairs per chunk
+    T = cuda_target(blobs_target(11, n, 8, n / 16, n / 6, Region.upper_half(n)))
+    lut = hb.lut_generate(LUT_SEED, 1 << 16)
+    runs = [hb.ospr_generate(T, 7, lut) for _ in range(3)]
+    for r in runs[1:]:
+        assert torch.equal(r.bits, runs[0].bits) and torch.equal(r.intensity, runs[0].intensity)
+        assert torch.equal(r.mse, runs[0].mse)
