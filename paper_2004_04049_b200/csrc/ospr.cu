@@ -57,7 +57,7 @@ __device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, 
     return (uint32_t)(((uint64_t)off_mod + (s % L) * (uint64_t)p_mod) % L);
 }
 
-// Z at the pixel pair {p1, p2 = -p1} of one sub-frame pair (a, b) from T (t1, t2) and the
+// conj(Z) at the pixel pair {p1, p2 = -p1} of one sub-frame pair (a, b) from T (t1, t2) and the
 // phase factors a1, a2 (sub-frame a) and b1, b2 (sub-frame b) at p1, p2.
 struct ZPair {
     float2 z1, z2;
@@ -68,8 +68,10 @@ __device__ __forceinline__ ZPair z_pair(float t1, float t2, float tb1, float tb2
     // Ha = t1 a1 + t2 conj(a2),  Hb = tb1 b1 + tb2 conj(b2)  (tb = t, or 0 for an absent b)
     const float2 ha = f2::fma(conjf2(a2), f2::bc(t2), f2::mul(a1, f2::bc(t1)));
     const float2 hb = f2::fma(conjf2(b2), f2::bc(tb2), f2::mul(b1, f2::bc(tb1)));
-    // Z(p) = Ha + i Hb,  Z(-p) = conj(Ha) + i conj(Hb) = (Ha.x + Hb.y, Hb.x - Ha.y)
-    return ZPair{cadd(ha, cmul_i(hb)), cadd(conjf2(ha), make_float2(hb.y, hb.x))};
+    // Z(p) = Ha + i Hb,  Z(-p) = conj(Ha) + i conj(Hb) = (Ha.x + Hb.y, Hb.x - Ha.y); returned
+    // CONJUGATED (sign flips folded into the adds' operand modifiers): pass A transforms
+    // conj(Z) with the forward body, F^-1{Z} = conj(F{conj(Z)}).
+    return ZPair{cadd(conjf2(ha), make_float2(-hb.y, -hb.x)), cadd(ha, make_float2(hb.y, -hb.x))};
 }
 
 // LUT index base of row y of a sub-frame whose draws start at base: (base + y N) mod L.
@@ -237,17 +239,15 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
             float2 *sg = sl + (size_t)slot * P::SMEM;
             float2 v[E];
 #pragma unroll
-            for (int m = 0; m < E; ++m) {
-                v[m] = sg[t + R1 * m];
-                v[m].y = -v[m].y;
-            }
+            for (int m = 0; m < E; ++m)
+                v[m] = sg[t + R1 * m];                       // conj(Z), built so by the producer
             fft::fft2pass<N, false, 1, true>(v, sg, t, twr);
             const int k = k0 + slot / 2;
             const int y = (slot & 1) ? (k > 0 ? N - k : N / 2) : k;
             float2 *o = buf + ((size_t)pair * N + y) * N;
 #pragma unroll
             for (int m = 0; m < E; ++m)
-                o[t + R1 * m] = make_float2(v[m].x, -v[m].y);
+                o[t + R1 * m] = v[m];   // conj of the row IFFT (the pair buffer is kept conjugated)
         }
         __syncwarp();
     }
@@ -356,15 +356,13 @@ ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
         float2 *sg = h ? s1 : s0;
         float2 v[E];
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-            v[m] = sg[t + R1 * m];
-            v[m].y = -v[m].y;
-        }
+        for (int m = 0; m < E; ++m)
+            v[m] = sg[t + R1 * m];                           // conj(Z), built so by the producer
         fft::fft2pass<N, false, 1, true>(v, sg, t, twp);
         float2 *o = buf + ((size_t)pair * N + (h ? ym : y)) * N;
 #pragma unroll
         for (int m = 0; m < E; ++m)
-            o[t + R1 * m] = make_float2(v[m].x, -v[m].y);
+            o[t + R1 * m] = v[m];       // conj of the row IFFT (the pair buffer is kept conjugated)
         asm volatile("bar.sync %0, 64;" ::"r"(1 + up) : "memory");   // both rows read before reuse
     }
 }
@@ -404,14 +402,10 @@ struct OsprColBody {
         Word *sw = reinterpret_cast<Word *>(scratch);            // [frame 2][t R1][c W] sign words
         Word wa = 0, wb = 0;                                     // a4: bit r = sign of row t + R1*r
         // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})
-        // exactly, since negation is exact.
+        // exactly, since negation is exact.  Pass A stores the conjugate of its row IFFT, so the
+        // tile already holds conj(x) and the column IFFT needs no input negation.
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-            if (h == 0) {
-#pragma unroll
-                for (int r = 0; r < E; ++r)
-                    v[r].y = -v[r].y;
-            }
             fft.template run<false, W>(v, sm, t);
             if (h == 0) {                                        // v = conj(H) (x N): Re H = v.x, Im H = -v.y
                 // u = (Re H, Im H) + 0 (one FADD2): -0.0 becomes +0.0, so u's sign bit is set iff
