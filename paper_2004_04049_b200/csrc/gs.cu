@@ -89,7 +89,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
         } else {
             R = make_float2(t, 0.0f);
         }
-        S[p] = R;
+        S[p] = conjf2(R);   // the state is kept conjugated (row passes transform conj(R) forward)
         const int y = p / N, x = p % N;
         if (in_region(y, x, om)) {
             const double td = t, t2 = td * td;
@@ -121,14 +121,10 @@ struct GsColBody {
         const size_t fofs = (size_t)fr * N * N;
         const int levels = a.levels;
         const float q_over_2pi = (float)levels * 0.15915494309189533577f;
-        // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})
+        // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)});
+        // the state is kept conjugated by the row passes, so the tile already holds conj(x)
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-            if (h == 0) {
-#pragma unroll
-                for (int r = 0; r < E; ++r)
-                    v[r].y = -v[r].y;
-            }
             fft.template run<false, W>(v, sm, t);
             if (h == 1)
                 break;
@@ -228,16 +224,14 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
 #pragma unroll
                 for (int r = 0; r < E; ++r)
                     tv[r] = __ldg(T + rofs + t + R1 * r);       // in flight during the FFT
-            } else {
-#pragma unroll
-                for (int r = 0; r < E; ++r)
-                    v[r].y = -v[r].y;
             }
-            fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);   // h = 0: X = N R'_k
+            // h = 0: X = N R'_k;  h = 1: F{conj(R_k)} = N conj(F^-1{R_k}), stored as is (the state
+            // is kept conjugated; the column pass then needs no input negation)
+            fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);
             if (h == 1) {
 #pragma unroll
                 for (int r = 0; r < E; ++r)
-                    state[rofs + t + R1 * r] = make_float2(v[r].x, -v[r].y);
+                    state[rofs + t + R1 * r] = v[r];
                 break;
             }
             // g4 metrics: fp32 partial sums over this thread's E elements (unbiased rounding, a
@@ -266,9 +260,8 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                     if (inten != nullptr)
                         inten[rofs + x] = I;
                 }
-                if (MODE != GS_LAST)
-                    v[r] = nz ? f2::mul(X, f2::bc(__fmul_rn(tt, rr)))          // R = T X / |X|
-                                     : make_float2(tt, 0.0f);                   // R-16: |R'| = 0 -> T
+                if (MODE != GS_LAST)   // conj(R_k), R_k = T X / |X| (R-16: |R'| = 0 -> T)
+                    v[r] = nz ? f2::mul(conjf2(X), f2::bc(__fmul_rn(tt, rr))) : make_float2(tt, -0.0f);
             }
             sums[0] = (double)sI;
             sums[1] = (double)sII;
@@ -293,7 +286,7 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
             if (MODE == GS_STEP) {
 #pragma unroll
                 for (int r = 0; r < E; ++r)
-                    r_out[rofs + t + R1 * r] = v[r];
+                    r_out[rofs + t + R1 * r] = conjf2(v[r]);   // R_k itself
             }
         }
         tma::fence_proxy_async_smem();
@@ -426,7 +419,7 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                         target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
                         r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state,
                         w.tparts + (size_t)g0 * kGsTBlocks * 2));
-        HOLO_TRY((launch_rows_fft<N, true>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));
+        HOLO_TRY((launch_rows_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));   // F{conj(R_0)}
         for (int k = 0; k < iters; ++k) {
             const bool last = (k == iters - 1);
             if (levels == 0) {
