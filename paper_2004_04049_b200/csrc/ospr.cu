@@ -651,6 +651,15 @@ __device__ __forceinline__ void block_reduce_store(double (&s)[5], int nvals, do
     }
 }
 
+// Finalize grid: FB CTAs of kFinThreads threads, ITER pixels per thread (fixed per N, so the
+// partial-sum order -- and the MSE -- is deterministic).
+template <int N>
+struct FinPlan {
+    static constexpr int P = N * N, WANT = (P + 8 * kFinThreads - 1) / (8 * kFinThreads);
+    static constexpr int FB = WANT < kFinBlocks ? WANT : kFinBlocks;
+    static constexpr int ITER = (P + FB * kFinThreads - 1) / (FB * kFinThreads);
+};
+
 // R-12 from the five fp64 sums: a = S_T2 / S_I (0 if S_I = 0);
 // mse = (a^2 S_II - 2 a S_IT2 + S_T4) / |Omega|.
 __device__ __forceinline__ double mse_from_sums(const double *o, double inv_count)
@@ -669,19 +678,18 @@ __device__ __forceinline__ double mse_from_sums(const double *o, double inv_coun
 template <int N>
 __global__ void __launch_bounds__(kFinThreads)
 ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T, int symmetrise, float scale,
-                     float *__restrict__ out, holo_region om, double *__restrict__ parts, unsigned *counter, double inv_count,
-                     double *__restrict__ mse, int fb, const uint8_t *__restrict__ bt, uint8_t *__restrict__ bits)
+                     float *__restrict__ out, holo_region om, double *__restrict__ parts, unsigned *counter,
+                     double inv_count, double *__restrict__ mse)
 {
     HOLO_PDL_ENTRY();
-    if ((int)blockIdx.x >= fb) {
-        const int j = (int)blockIdx.x - fb;
-        bits_transpose_block<N>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
-        return;
-    }
-    constexpr int P = N * N, LOG = fft::ilog2(N);
+    constexpr int P = N * N, LOG = fft::ilog2(N), FB = FinPlan<N>::FB, ITER = FinPlan<N>::ITER;
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-    for (int k = blockIdx.x * kFinThreads + threadIdx.x; k < P; k += fb * kFinThreads) {
+    // a fixed number of pixels per thread, fully unrolled: every load is in flight at once
+#pragma unroll
+    for (int i = 0; i < ITER; ++i) {
+        const int k = (int)blockIdx.x * kFinThreads + (int)threadIdx.x + i * FB * kFinThreads;
+        if (k >= P)
+            break;
         const int y = k >> LOG, x = k & (N - 1);
         float I;
         if (symmetrise) {
@@ -708,14 +716,14 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
     __shared__ int last;
     if (threadIdx.x == 0) {
         __threadfence();                                   // this CTA's slot before its ticket
-        last = atomicAdd(counter, 1u) == (unsigned)fb - 1;
+        last = atomicAdd(counter, 1u) == (unsigned)FB - 1;
     }
     __syncthreads();
     if (!last)
         return;
     __threadfence();
     double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int b = threadIdx.x; b < fb; b += blockDim.x)
+    for (int b = threadIdx.x; b < FB; b += blockDim.x)
         for (int i = 0; i < 5; ++i)
             t[i] += __ldcg(parts + (size_t)b * 5 + i);
     __shared__ double o[5];
@@ -781,19 +789,12 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
 // The completion ticket of the finalize kernel, after its per-CTA partial-sum slots.
 static unsigned *finalize_ticket(double *parts) { return reinterpret_cast<unsigned *>(parts + (size_t)kFinBlocks * 5); }
 
-static int fin_grid(int n)
-{
-    const int want = (n * n + 7 * kFinThreads - 1) / (7 * kFinThreads);   // about 7 pixels per thread
-    return want < kFinBlocks ? want : kFinBlocks;
-}
 
 // Finalize one frame (and, if bits != NULL, transpose its nq sub-frames of sign bytes).
 template <int N>
 holo_status finalize_frame(const float *acc, const float *T, int symmetrise, float scale, float *out, holo_region om,
-                           double *parts, double *mse, const uint8_t *bt, uint8_t *bits, int nq, cudaStream_t s,
-                           bool ticket_zeroed = false)
+                           double *parts, double *mse, cudaStream_t s, bool ticket_zeroed = false)
 {
-    const int fb = fin_grid(N);
     unsigned *counter = finalize_ticket(parts);
     const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
     if (mse && !ticket_zeroed) {
@@ -801,9 +802,8 @@ holo_status finalize_frame(const float *acc, const float *T, int symmetrise, flo
         if (e != cudaSuccess)
             return cuda_status(e, "cudaMemsetAsync(finalize ticket)");
     }
-    const int nbt = bits ? nq * BitsT<N>::BLOCKS_PER_Q : 0;
-    return launch(K_OSPR_FINALIZE, ospr_finalize_kernel<N>, dim3(fb + nbt), dim3(kFinThreads), 0, s, acc, T,
-                  symmetrise, scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse, fb, bt, bits);
+    return launch(K_OSPR_FINALIZE, ospr_finalize_kernel<N>, dim3(FinPlan<N>::FB), dim3(kFinThreads), 0, s, acc, T,
+                  symmetrise, scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse);
 }
 
 template <int N>
@@ -870,7 +870,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
         }
         const float scale = full ? 0.5f / (float)n_sub : 0.5f;
         HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
-                                   (full && mse) ? mse + f : nullptr, nullptr, nullptr, 0, s, true));
+                                   (full && mse) ? mse + f : nullptr, s, true));
     }
     return HOLO_OK;
 }
@@ -995,7 +995,7 @@ extern "C" holo_status holo_ospr_finalize(const float *target, const float *inte
         double *m = mse ? mse + f : nullptr, *parts = (double *)ws;
 #define HOLO_FIN_CASE(NN)                                                                                  \
     case NN:                                                                                               \
-        HOLO_TRY(finalize_frame<NN>(a, t, 0, 1.0f / (float)n_sub, o, omega, parts, m, nullptr, nullptr, 0, s)); \
+        HOLO_TRY(finalize_frame<NN>(a, t, 0, 1.0f / (float)n_sub, o, omega, parts, m, s)); \
         break;
         switch (n) {
             HOLO_FIN_CASE(16)
