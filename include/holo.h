@@ -19,6 +19,12 @@
  *    enqueued; results are valid once the stream has completed.
  *  - Calls are thread-safe across distinct workspaces and streams.  Two
  *    calls sharing a workspace must be ordered by the caller.
+ *  - Kernels are launched with programmatic stream serialisation (PDL): a
+ *    kernel may be scheduled while its predecessor in the stream drains, but
+ *    waits for it to complete before touching memory, so stream order is
+ *    kept exactly (HOLO_PDL=0 in the environment launches them plainly).
+ *    Every call may be captured into a CUDA graph after a first eager call
+ *    on the device.
  *  - Images are row-major data[y][x], x fastest (R-10); complex values are
  *    interleaved (re, im) fp32 pairs (`holo_c64`); DC is at [0][0] with no
  *    shift (R-10); the DFT pair is unitary, 1/sqrt(Nx*Ny) in both
