@@ -2,20 +2,23 @@
 // steps a1-a7 of DESIGN.md §1) as three fused FFT passes per chunk of
 // sub-frame pairs plus a finalize pass per frame.
 //
-//   pass A  ospr_rows_a  R_s = T * lut[(base_s + p) mod L] for the two sub-frames
-//                        a, b of a pair at pixels p and -p, Hermitian parts packed
-//                        as Z = 2 Herm(R_a) + 2i Herm(R_b) (so F^-1{Z} =
-//                        2 (Re H_a + i Re H_b)), built in shared
-//                        memory and row-IFFTed in the same kernel.
+//   pass A  ospr_rows_a(2)  R_s = T * lut[(base_s + p) mod L] (or the on-the-fly
+//                        source, LUT_PRNG) for the two sub-frames a, b of a pair at
+//                        pixels p and -p, Hermitian parts packed as Z = 2 Herm(R_a)
+//                        + 2i Herm(R_b) (so F^-1{Z} = 2 (Re H_a + i Re H_b),
+//                        DESIGN.md §5), built (conjugated) in shared memory and
+//                        row-IFFTed in the same kernel; N >= 1024: a warp pair per
+//                        mirrored row pair (ospr_rows_a2_kernel).
 //   pass B  ospr_cols    column IFFT -> H; a4: bit_a = Re H >= 0, bit_b = Im H >= 0,
-//                        packed MSB-first via warp ballots; h' = (+-1) + i(+-1);
-//                        column FFT of h'; write back in place.
+//                        8x8 bit transposes into tile-major sign bytes;
+//                        h' = (+-1) + i(+-1); column FFT of h'; TMA store in place.
 //   pass C  ospr_rows_c  row FFT -> X = F{h'_a} + i F{h'_b}; accumulate |X|^2/N^2
 //                        over the chunk's pairs in registers; one RMW of the
-//                        frame accumulator A per chunk.
+//                        frame accumulator A per chunk; on the frame's last chunk
+//                        extra CTAs turn the sign bytes into packed holograms (R-8).
 //   finalize             I[k] = (A[k] + A[-k]) / 2 / N_SF  (= sum_s |F{h'_s}|^2 / N_SF,
-//                        DESIGN.md §5), the fp64 MSE over Omega, and the packed
-//                        holograms (tile-major sign bytes -> row-major, R-8).
+//                        DESIGN.md §5) and the fp64 MSE over Omega (last-CTA
+//                        fixed-order reduction).
 //
 // All 1/sqrt(N) factors of Eqs. (1)-(2) are dropped inside the passes: a positive
 // scale does not change sign(Re H), and the forward scale 1/N^2 on |X|^2 is an
