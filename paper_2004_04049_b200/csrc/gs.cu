@@ -128,11 +128,11 @@ struct GsColBody {
             fft.template run<false, W>(v, sm, t);
             if (h == 1)
                 break;
+            int jl[QUANT ? E : 1];                             // level indices (QUANT)
 #pragma unroll
             for (int r = 0; r < E; ++r) {
                 const float2 hk = make_float2(v[r].x, -v[r].y);  // H_k (x N)
                 float2 o;
-                int j = 0;
                 if constexpr (!QUANT) {
                     const float m2 = __fmaf_rn(hk.x, hk.x, __fmul_rn(hk.y, hk.y));
                     o = m2 < kFltMin ? make_float2(1.0f, 0.0f)               // R-16: H = 0 -> +1
@@ -141,17 +141,26 @@ struct GsColBody {
                     float th = atan2f(hk.y, hk.x);
                     if (th < 0.0f)
                         th += 6.28318530717958647692f;
-                    j = (int)floorf(th * q_over_2pi + 0.5f);
+                    int j = (int)floorf(th * q_over_2pi + 0.5f);
                     if (j >= levels)
                         j -= levels;
+                    jl[r] = j;
                     o = a.qtab[j];                             // (cos, sin)(2 pi j / Q), built by gs_qtab
                 }
-                const size_t idx = fofs + (size_t)(t + R1 * r) * N + tile * W + c;
-                if (a.holo != nullptr)
-                    a.holo[idx] = o;
-                if (a.lev != nullptr)
-                    a.lev[idx] = (uint8_t)j;
                 v[r] = o;
+            }
+            if (a.holo != nullptr || a.lev != nullptr) {       // last iteration only: g6 outputs
+                const size_t base = fofs + (size_t)t * N + tile * W + c;
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const size_t idx = base + (size_t)R1 * r * N;
+                    if (a.holo != nullptr)
+                        a.holo[idx] = v[r];
+                    if constexpr (QUANT) {
+                        if (a.lev != nullptr)
+                            a.lev[idx] = (uint8_t)jl[r];
+                    }
+                }
             }
         }
         // (the pipeline stores v, the column FFT of h_k, with a TMA tile store)
