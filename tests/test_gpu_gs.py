@@ -163,3 +163,16 @@ def test_gs_groups_bit_identical(monkeypatch):
     assert hb.gs_group_frames(n, B) == 2
     b = hb.gs_generate(T, iters, lut, levels=0)
     assert torch.equal(a.mse, b.mse) and torch.equal(a.holo, b.holo) and torch.equal(a.intensity, b.intensity)
+
+
+@pytest.mark.parametrize("n", [512, 2048])
+def test_gs_large_sizes_one_iteration(n):
+    """GS at the sizes the fixed configurations skip (512: two-pass rows with E = 16 values;
+    2048: the single-stage column pipeline and E = 64): first-iteration MSE and E_1 against
+    the oracle, continuous and 8-level constraints."""
+    T = blobs_target(4242 + n, n, 8, n / 32, n / 8, Region.full(n))
+    lg, lo = lut_pair(LUT_SEED, 4099)
+    for Q in (0, 8):
+        res = hb.gs_generate(cuda_target(T[None]), 1, lg, phase_offset=77, levels=Q)
+        ref = oracle.gs(T, 1, lo, 77, Q, (0, n, 0, n))
+        assert rel(to_np(res.mse)[0, 0], ref["mse"][0]) <= REL_TOL, (n, Q)
