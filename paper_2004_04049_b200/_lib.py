@@ -66,6 +66,8 @@ SIGNATURES = {
 def lib():
     """Load libholo.so (raising if it is absent: there is no fallback path)."""
     global _lib
+    if _lib is not None:                 # fast path: no lock once loaded
+        return _lib
     with _lock:
         if _lib is None:
             if not os.path.exists(LIB_PATH):

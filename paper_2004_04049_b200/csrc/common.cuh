@@ -50,6 +50,9 @@ void prof_before(KernelId id, cudaStream_t s);
 void prof_after(KernelId id, cudaStream_t s);
 void count_launch();
 holo_status ensure_smem(const void *fn, size_t smem);
+// SMs x resident CTAs per SM of `fn` at (threads, smem) on the current device; cached, and
+// opts the kernel in to `smem` bytes of dynamic shared memory first.
+int resident_ctas(const void *fn, int threads, size_t smem);
 
 // Programmatic dependent launch (PDL): every library kernel is launched with programmatic
 // stream serialisation and begins with HOLO_PDL_ENTRY: it waits for the previous kernel in

@@ -117,16 +117,8 @@ rows_fft_kernel(const float2 *__restrict__ tw, const float2 *in, float2 *out, in
 template <typename K>
 inline int pipe_grid(K kernel, int threads, size_t smem, int nitems, int wpc)
 {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (smem > 0)
-        ensure_smem((const void *)kernel, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-    if (per_sm < 1)
-        per_sm = 1;
+    const int cap = resident_ctas((const void *)kernel, threads, smem);   // SMs x CTAs per SM (cached)
     const int want = (nitems + wpc - 1) / wpc;
-    const int cap = sms * per_sm;
     return want < cap ? want : cap;
 }
 

@@ -9,6 +9,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -138,6 +139,31 @@ holo_status ensure_smem(const void *fn, size_t smem)
         return cuda_status(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
     g_smem_done.insert(key);
     return HOLO_OK;
+}
+
+static std::mutex g_occ_mu;
+static std::map<std::tuple<int, const void *, int, size_t>, int> g_occ;
+
+int resident_ctas(const void *fn, int threads, size_t smem)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, fn, threads, smem);
+    {
+        std::lock_guard<std::mutex> lk(g_occ_mu);
+        auto it = g_occ.find(key);
+        if (it != g_occ.end())
+            return it->second;
+    }
+    if (smem > 0)
+        ensure_smem(fn, smem);
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    const int cap = sms * (per_sm < 1 ? 1 : per_sm);
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    g_occ[key] = cap;
+    return cap;
 }
 
 namespace fft {
