@@ -237,6 +237,34 @@ def kernel_times(hb, step_fn, steps, flush, use_graph):
     return {k: {"launches": v[0], "total_ms": v[1], "avg_us": 1e3 * v[1] / v[0]} for k, v in acc.items()}
 
 
+def graphed_stages(pre, collective, post, enabled):
+    """A step made of two local parts around one collective: pre and post are each captured
+    into a CUDA graph (after one eager run), the collective (NCCL) runs eagerly between them."""
+    if not enabled:
+        def eager():
+            pre()
+            collective()
+            post()
+        return eager
+    import torch
+    pre()
+    collective()
+    post()
+    torch.cuda.synchronize()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1):
+        pre()
+    with torch.cuda.graph(g2):
+        post()
+    torch.cuda.synchronize()
+
+    def replay():
+        g1.replay()
+        collective()
+        g2.replay()
+    return replay
+
+
 def run_gpu(args):
     import torch
     import paper_2004_04049_b200 as hb
@@ -255,8 +283,12 @@ def run_gpu(args):
     n, S, P = w3.n, w3.n_sub, w3.n * w3.n
     T = torch.from_numpy(target_for(w3)).to(dev)
     from paper_2004_04049_b200.parallel import shard_range
-    sb, se = shard_range(S, world, rank)
-    full = (world == 1)
+    # HOLO_BENCH_FAKE_WORLD=k (testing only, N = 1): run rank 0's shard of a k-way split with a
+    # no-op collective, to exercise the N > 1 step structure (graphs around the collective)
+    fake = int(os.environ.get("HOLO_BENCH_FAKE_WORLD", "0")) if world == 1 else 0
+    sworld = fake if fake > 1 else world
+    sb, se = shard_range(S, sworld, rank)
+    full = (sworld == 1)
     ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device=dev)
     lut_buf = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
     out = hb.OsprResult(bits=torch.empty((1, se - sb, n, n // 8), dtype=torch.uint8, device=dev),
@@ -266,24 +298,33 @@ def run_gpu(args):
     mse_buf = torch.empty(1, dtype=torch.float64, device=dev)
 
     from paper_2004_04049_b200.parallel import ShardedOspr
-    sharded = ShardedOspr(world, rank)
+    sharded = ShardedOspr(sworld, rank, all_reduce=(lambda t: None)) if fake > 1 else ShardedOspr(world, rank)
+
+    def ospr_stages(L, lut, T_in=None):
+        """(pre, C-1, post) of one OSPR step: a0 + this rank's shard, the all-reduce of the
+        partial intensity (N > 1), then mean + MSE (a7)."""
+        pre, coll, post = sharded.stages(T if T_in is None else T_in, S, lut[:L], ws, out, mse_buf)
+
+        def pre_a0():
+            hb.lut_generate(LUT_SEED, L, out=lut[:L])                               # a0
+            pre()                                                                   # a1-a6 (shard)
+        return pre_a0, coll, post
 
     def make_ospr_step(L, lut):
+        pre, coll, post = ospr_stages(L, lut)
+
         def step():
-            hb.lut_generate(LUT_SEED, L, out=lut[:L])                               # a0
-            if full:
-                hb.ospr_generate(T, S, lut[:L], workspace=ws, out=out)              # a1-a7
-            else:
-                r = sharded.run(T, S, lut[:L], workspace=ws)                        # a1-a6 shard, C-1, a7
-                out.mse = r.mse
+            pre()
+            coll()                                                                  # C-1 (NCCL), N > 1
+            post()                                                                  # a7
         return step
 
+    use_graph = not args.no_graph
     step = make_ospr_step(args.lut, lut_buf)
-    use_graph = not args.no_graph and world == 1
     l0 = hb.launch_count()
     step()
     launches_per_step = hb.launch_count() - l0                 # libholo kernels in one step
-    timed_step = graphed(step, use_graph)
+    timed_step = graphed_stages(*ospr_stages(args.lut, lut_buf), use_graph)
     with Clocks(local) as clk:
         total_ms, per = timed_loop(timed_step, args.steps, args.warmup, world, flush)
     launches_timed = launches_per_step * args.steps
@@ -293,7 +334,7 @@ def run_gpu(args):
 
     # per-kernel device time: the same step in the same launch configuration, every kernel
     # bracketed by CUDA events on its launch stream, K more steps after an L2 flush each
-    kern = kernel_times(hb, step, args.steps, flush, use_graph)
+    kern = kernel_times(hb, step, args.steps, flush, use_graph and world == 1)   # (no NCCL in a graph)
     step_kernel_ms = sum(v["total_ms"] for v in kern.values()) / args.steps
 
     # roofline of the dominant kernel (algorithmic bytes per launch)
@@ -329,7 +370,8 @@ def run_gpu(args):
                                "a1-a7 incl. MSE); BASELINE configs[2]",
                    "n": n, "n_sub": S, "lut_len": args.lut, "lut_seed": LUT_SEED,
                    "l2": "flushed before every timed step (256 MiB write)",
-                   "launch": "CUDA graph replay of the step (captured once)" if use_graph else "eager launches",
+                   "launch": ("CUDA graph replay of the step (captured once)" if world == 1 else
+                              "CUDA graph replays around the eager NCCL all-reduce") if use_graph else "eager launches",
                    "parallelism": f"sub-frame shards x{world}" + (" + NCCL all-reduce of intensity" if world > 1 else "")},
         "gpu_launches": launches_timed,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -372,24 +414,24 @@ def run_gpu(args):
         T_dev = torch.empty_like(T)
         lut_e2e = hb.lut_generate(LUT_SEED, args.lut, device=dev)
 
-        def e2e_step():
+        pre, coll, post = ospr_stages(args.lut, lut_e2e, T_in=T_dev)
+
+        def e2e_pre():
             T_dev.copy_(T_host, non_blocking=True)                              # H2D inputs
-            hb.lut_generate(LUT_SEED, args.lut, out=lut_e2e)                    # a0
-            if full:
-                hb.ospr_generate(T_dev, S, lut_e2e, workspace=ws, out=out)
-                mse_host.copy_(out.mse, non_blocking=True)                      # D2H metric
-                bits_host.copy_(out.bits, non_blocking=True)                    # D2H holograms
-            else:
-                r = sharded.run(T_dev, S, lut_e2e, workspace=ws)
-                mse_host.copy_(r.mse, non_blocking=True)
-                bits_host.copy_(r.bits, non_blocking=True)
-        tm, _ = timed_loop(graphed(e2e_step, use_graph), args.steps, args.warmup, world, flush)
+            pre()                                                               # a0, a1-a6 (shard)
+
+        def e2e_post():
+            post()                                                              # a7
+            mse_host.copy_(mse_buf, non_blocking=True)                          # D2H metric
+            bits_host.copy_(out.bits, non_blocking=True)                        # D2H holograms
+        tm, _ = timed_loop(graphed_stages(e2e_pre, coll, e2e_post, use_graph), args.steps, args.warmup, world,
+                           flush)
         tm = max_over_ranks(tm, world)
         result["e2e"] = {"value": S * args.steps / (tm / 1e3), "unit": UNIT,
                          "h2d_bytes_per_step": T_host.numel() * 4,
                          "d2h_bytes_per_step": bits_host.numel() + 8,
                          "what": "pinned host target -> device, a0 LUT build, ospr_generate (a1-a7), packed "
-                                 "holograms + MSE -> host; " + ("one CUDA graph per step (memcpy + kernel nodes)"
+                                 "holograms + MSE -> host; " + ("CUDA graphs (memcpy + kernel nodes)"
                                                                 if use_graph else "eager")}
 
     # ---------------- GS C4 ----------------

@@ -135,16 +135,21 @@ def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] 
 
 def ospr_finalize(target: torch.Tensor, intensity_sum: torch.Tensor, n_sub: int,
                   omega: Optional[Sequence[int]] = None, want_mse: bool = True,
-                  out: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
-    """Mean intensity (= sum / n_sub; in place if out is intensity_sum) and MSE."""
+                  out: Optional[torch.Tensor] = None, mse_out: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
+    """Mean intensity (= sum / n_sub; in place if out is intensity_sum) and MSE.  Passing
+    mse_out and workspace makes the call allocation-free (CUDA-graph capturable)."""
     _need(target, torch.float32, "target")
     _need(intensity_sum, torch.float32, "intensity_sum")
     t3 = target if target.dim() == 3 else target.unsqueeze(0)
     F, n, _ = t3.shape
     om = omega if omega is not None else default_omega(n, "ospr")
     out = torch.empty_like(intensity_sum) if out is None else out
-    mse = torch.empty(F, dtype=torch.float64, device=t3.device) if want_mse else None
-    ws = torch.empty(int(lib().holo_ospr_finalize_workspace_size()), dtype=torch.uint8, device=t3.device)
+    mse = (mse_out if mse_out is not None else torch.empty(F, dtype=torch.float64, device=t3.device)) \
+        if want_mse else None
+    need = int(lib().holo_ospr_finalize_workspace_size())
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(need, dtype=torch.uint8, device=t3.device)
     check(lib().holo_ospr_finalize(t3.data_ptr(), intensity_sum.data_ptr(), n, F, n_sub, _region(om),
                                    out.data_ptr(), _ptr(mse), ws.data_ptr(), ws.numel(), _stream(t3.device)))
     return out, mse

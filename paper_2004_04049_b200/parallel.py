@@ -59,6 +59,36 @@ class ShardedOspr:
         self.world, self.rank = world, rank
         self.generate, self.finalize, self.all_reduce = generate, finalize, all_reduce
 
+    def stages(self, target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor], workspace: torch.Tensor,
+               out, mse_out: Optional[torch.Tensor], phase_offset: int = 0, omega=None):
+        """The step split around its one collective, for CUDA-graph capture of the two local
+        parts: (pre, collective, post).  pre: this rank's shard into out (bits and the partial
+        intensity sum); collective: C-1 on out.intensity; post: mean and MSE in place (a
+        single rank skips the collective).  All buffers are caller-owned, so pre and post
+        allocate nothing."""
+        b, e = shard_range(n_sub, self.world, self.rank)
+        if b == e:
+            raise ValueError("more ranks than sub-frames: use run()")
+        if self.world == 1:                          # the whole range: mean and MSE in one call
+            def whole():
+                out.mse = mse_out
+                self.generate(target, n_sub, lut, phase_offset=phase_offset, omega=omega, workspace=workspace,
+                              out=out)
+            return whole, (lambda: None), (lambda: None)
+
+        def pre():
+            self.generate(target, n_sub, lut, phase_offset=phase_offset, sf_range=(b, e), want_mse=False,
+                          omega=omega, workspace=workspace, out=out)
+
+        def collective():
+            if self.world > 1:
+                self.all_reduce(out.intensity)
+
+        def post():
+            api.ospr_finalize(target, out.intensity, n_sub, omega=omega, out=out.intensity, mse_out=mse_out,
+                              workspace=workspace)
+        return pre, collective, post
+
     def run(self, target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor], phase_offset: int = 0,
             want_bits: bool = True, want_mse: bool = True, omega=None, workspace=None) -> ShardedOsprResult:
         b, e = shard_range(n_sub, self.world, self.rank)
