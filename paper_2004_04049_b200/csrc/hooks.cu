@@ -8,17 +8,18 @@ namespace holo {
 template <int N, bool INV>
 struct HookColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
+    static constexpr int kWidth = 8;   // columns per tile
     struct Args {
         const float2 *tw;
         float2 *buf;
         float scale;
     };
-    template <class F>
+    template <class F, int W>
     static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *, int c, int t, int fr,
                                                int tile,
                                                const Args &a, const F &fft)
     {
-        constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
+        constexpr int R1 = F::T, E = F::E;   // element m of thread t = row t + R1*m; W columns per tile
         fft.template run<INV, W>(v, sm, t);
 #pragma unroll
         for (int r = 0; r < E; ++r)

@@ -386,6 +386,7 @@ __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
 template <int N>
 struct OsprColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
+    static constexpr int kWidth = 8;   // columns per tile
     struct Args {
         const float2 *tw;
         float2 *buf;
@@ -393,15 +394,15 @@ struct OsprColBody {
         int npairs;
         int last_has_b;
     };
-    template <class F>
+    template <class F, int W>
     static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *scratch, int c, int t,
                                                int pair, int ct, const Args &a, const F &fft)
     {
-        constexpr int R1 = F::T, E = F::E, W = ColPipe<N>::W;   // element m of thread t = row t + R1*m
+        constexpr int R1 = F::T, E = F::E;   // element m of thread t = row t + R1*m; W columns per tile
         const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
         static_assert(E <= 64 && W == 8, "bit words hold at most 64 rows per thread; one byte per tile row");
         using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
-        static_assert(2 * W * R1 * sizeof(Word) <= ColPipe<N>::SCRATCH_BYTES, "scratch holds both bit planes");
+        static_assert(2 * W * R1 * sizeof(Word) <= ColPipe<N, 0, W>::SCRATCH_BYTES, "scratch holds both bit planes");
         Word *sw = reinterpret_cast<Word *>(scratch);            // [frame 2][t R1][c W] sign words
         Word wa = 0, wb = 0;                                     // a4: bit r = sign of row t + R1*r
         // IFFT then FFT through ONE transform body (instruction cache): F^-1{x} = conj(F{conj(x)})

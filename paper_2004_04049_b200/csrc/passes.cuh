@@ -141,9 +141,9 @@ struct ColFftFor {
     using type = fft::ColFft2<N, REG>;
 };
 
-template <int N, int NSTAGES = 0>
+template <int N, int NSTAGES = 0, int WIDTH = 8>
 struct ColPipe {
-    static constexpr int W = 8;                            // columns per tile (= one packed byte per row)
+    static constexpr int W = WIDTH;                        // columns per tile (OSPR: 8 = one packed byte per row)
     // 3 stages: one CTA per SM, tile k+2 loading while tile k computes and tile k-1's store
     // drains; 1 stage: two CTAs per SM overlap each other's loads and stores
     static constexpr int STAGES = NSTAGES > 0 ? NSTAGES : 3;
@@ -171,11 +171,12 @@ struct ColPipe {
 // back through the stage and one TMA tile store (in place); a stage is refilled once
 // its store has been read out, PREFETCH tiles ahead.
 template <int N, class Body, int NSTAGES>
-__global__ void __launch_bounds__(ColPipe<N, NSTAGES>::THREADS, (ColPipe<N, NSTAGES>::STAGES == 1 && N <= 1024) ? 2 : 1)
+__global__ void __launch_bounds__(ColPipe<N, NSTAGES, Body::kWidth>::THREADS,
+                                  ((ColPipe<N, NSTAGES, Body::kWidth>::STAGES == 1 && N <= 1024) || Body::kWidth < 8) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
 {
     HOLO_PDL_ENTRY();
-    using CP = ColPipe<N, NSTAGES>;
+    using CP = ColPipe<N, NSTAGES, Body::kWidth>;
     using F = typename CP::F;
     constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME, S = CP::STAGES, PF = CP::PREFETCH;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -215,7 +216,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
-        Body::template run<F>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
+        Body::template run<F, W>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
         // results -> the stage in natural [row][col] layout -> one TMA tile store (in place)
         __syncthreads();                   // every thread is done with the exchange data
 #pragma unroll
@@ -245,7 +246,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
 template <int N, class Body, int NSTAGES>
 holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
 {
-    using CP = ColPipe<N, NSTAGES>;
+    using CP = ColPipe<N, NSTAGES, Body::kWidth>;
     CUtensorMap map;
     HOLO_TRY(make_tmap_c64(&map, buf, N, (uint64_t)nframes * N, CP::W, CP::BOX_ROWS));
     // persistent grid: SMs x resident CTAs per SM (registers and shared memory both count)
