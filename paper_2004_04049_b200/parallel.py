@@ -85,8 +85,8 @@ class ShardedOspr:
                 self.all_reduce(out.intensity)
 
         def post():
-            api.ospr_finalize(target, out.intensity, n_sub, omega=omega, out=out.intensity, mse_out=mse_out,
-                              workspace=workspace)
+            self.finalize(target, out.intensity, n_sub, omega=omega, out=out.intensity, mse_out=mse_out,
+                          workspace=workspace)
         return pre, collective, post
 
     def run(self, target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor], phase_offset: int = 0,

@@ -38,7 +38,7 @@ def test_shard_range_partition():
 # ---- oracle-backed stand-ins for the libholo calls (test doubles) -----------------------------
 
 def oracle_ospr_generate(target, n_sub, lut, phase_offset=0, sf_range=None, want_bits=True, want_mse=True,
-                         omega=None, workspace=None):
+                         omega=None, workspace=None, out=None):
     T = target.numpy()
     T3 = T if T.ndim == 3 else T[None]
     F, n, _ = T3.shape
@@ -52,10 +52,15 @@ def oracle_ospr_generate(target, n_sub, lut, phase_offset=0, sf_range=None, want
             bi, _, I = oracle.ospr_subframe(T3[f], lo, cur, want_h=False, want_intensity=True)
             bits[f, s - b] = bi
             inten[f] += I
+    if out is not None:                  # write into the caller's buffers (graph-style API)
+        out.intensity.copy_(torch.from_numpy(inten))
+        out.bits.copy_(torch.from_numpy(bits))
+        return out
     return SimpleNamespace(intensity=torch.from_numpy(inten), bits=torch.from_numpy(bits), mse=None)
 
 
-def oracle_ospr_finalize(target, intensity_sum, n_sub, omega=None, want_mse=True, out=None):
+def oracle_ospr_finalize(target, intensity_sum, n_sub, omega=None, want_mse=True, out=None, mse_out=None,
+                         workspace=None):
     T = target.numpy()
     T3 = T if T.ndim == 3 else T[None]
     mean = intensity_sum / n_sub
@@ -65,6 +70,9 @@ def oracle_ospr_finalize(target, intensity_sum, n_sub, omega=None, want_mse=True
     region = omega or Region.upper_half(T3.shape[-1]).as_tuple()
     mse = torch.tensor([oracle.mse_m1(mean[f].numpy(), T3[f], region) for f in range(T3.shape[0])],
                        dtype=torch.float64)
+    if mse_out is not None:
+        mse_out.copy_(mse)
+        mse = mse_out
     return mean, mse
 
 
@@ -95,12 +103,22 @@ def _worker(rank, world, port, out_dir):
         sh = ShardedOspr(world, rank, generate=oracle_ospr_generate, finalize=oracle_ospr_finalize,
                          all_reduce=lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
         res = sh.run(torch.from_numpy(Ts), NSUB, lut, phase_offset=11)
+        # the bench's N > 1 step structure: (shard) -> C-1 -> (finalize) into caller-owned buffers
+        b, e = shard_range(NSUB, world, rank)
+        buf = SimpleNamespace(bits=torch.zeros((2, e - b, N, N // 8), dtype=torch.uint8),
+                              intensity=torch.zeros((2, N, N), dtype=torch.float64), mse=None)
+        mse_buf = torch.zeros(2, dtype=torch.float64)
+        pre, coll, post = sh.stages(torch.from_numpy(Ts), NSUB, lut, None, buf, mse_buf, phase_offset=11)
+        pre()
+        coll()
+        post()
         gTs = np.stack([blobs_target(70 + b, N, 3, 2.0, 5.0, Region.full(N)) for b in range(5)])
         (fb, fe), gres = ShardedGs(world, rank, generate=oracle_gs_generate).run(
             torch.from_numpy(gTs), 3, lut, phase_offset=5)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), b=res.sf_range[0], e=res.sf_range[1],
                  bits=res.bits.numpy(), inten=res.intensity.numpy(), mse=res.mse.numpy(),
-                 fb=fb, fe=fe, gmse=gres.mse.numpy())
+                 fb=fb, fe=fe, gmse=gres.mse.numpy(), st_bits=buf.bits.numpy(), st_inten=buf.intensity.numpy(),
+                 st_mse=mse_buf.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -120,6 +138,10 @@ def test_sharded_ospr_and_gs_gloo_world2(tmp_path):
         # every rank holds the all-reduced mean and the MSE computed after the reduction
         assert np.max(np.abs(o["inten"] - I_ref)) <= 1e-12 * I_ref.max()
         assert np.allclose(o["mse"], mse_ref, rtol=1e-12, atol=0)
+        # the staged form (pre / collective / post into caller buffers) gives the same result
+        assert np.array_equal(o["st_bits"], o["bits"])
+        assert np.max(np.abs(o["st_inten"] - I_ref)) <= 1e-12 * I_ref.max()
+        assert np.allclose(o["st_mse"], mse_ref, rtol=1e-12, atol=0)
     # GS: frames [0,2) and [2,5), initial phases drawn at the global cursor
     gTs = np.stack([blobs_target(70 + b, N, 3, 2.0, 5.0, Region.full(N)) for b in range(5)])
     full = np.stack([oracle.gs(gTs[b], 3, lo, 5 + b * N * N, 0, (0, N, 0, N))["mse"] for b in range(5)])
