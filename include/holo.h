@@ -228,6 +228,19 @@ holo_status holo_debug_randomise(const float *target, int32_t n, const holo_c64 
                                  uint64_t n_lut, uint64_t offset, holo_c64 *r_out,
                                  holo_stream stream);
 
+/* Test hook: pass A's randomisation stage alone (steps a1, a2 exactly as
+ * holo_ospr_generate runs them, same kernels with the FFT skipped).  For the
+ * sub-frames [sf_begin, sf_end) of frame 0, taken two at a time (a, b), writes
+ * z_out[pair][n][n] = conj(Z) with Z(p) = (R_a(p) + conj(R_a(-p))) +
+ * i (R_b(p) + conj(R_b(-p))), R_s = T * lut[(phase_offset + s n^2 + p) mod n_lut]
+ * (R_b = 0 for an unpaired last sub-frame): the Hermitian pairing of
+ * DESIGN.md §5.  use_prng != 0 (lut NULL): the phases of holo_ospr_generate_prng
+ * with stream prng_seed instead.  Errors as holo_ospr_generate. */
+holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int32_t n_sub, const holo_c64 *lut,
+                                  uint64_t n_lut, int32_t use_prng, uint64_t prng_seed,
+                                  uint64_t phase_offset, int32_t sf_begin, int32_t sf_end,
+                                  holo_c64 *z_out, holo_stream stream);
+
 /* One GS iteration (g1-g5) from r_in = R_{k-1} for `batch` frames: writes
  * r_out = R_k and, if non-NULL, holo = h_k, holo_levels, intensity = I_k,
  * mse[b], err_e[b].  Bit-identical to iteration k of holo_gs_generate when

@@ -20,7 +20,7 @@ from ._lib import HoloRegion, check, lib
 
 __all__ = [
     "lut_generate", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize", "gs_workspace_bytes",
-    "gs_generate", "gs_step", "fft2", "debug_randomise", "launch_count", "profile_enable", "profile_read",
+    "gs_generate", "gs_step", "fft2", "debug_randomise", "debug_ospr_pairs", "launch_count", "profile_enable", "profile_read",
     "kernel_names", "version", "default_omega", "OsprResult", "GsResult",
 ]
 
@@ -243,6 +243,22 @@ def debug_randomise(target: torch.Tensor, lut: Optional[torch.Tensor], offset: i
 
 
 # ---- instrumentation -------------------------------------------------------------------------------------
+
+def debug_ospr_pairs(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor], offset: int = 0,
+                     sf_range: Optional[Tuple[int, int]] = None, prng_seed: Optional[int] = None) -> torch.Tensor:
+    """Test hook: pass A's randomisation (conj of the Hermitian-paired Z) for frame 0's
+    sub-frame pairs in sf_range; complex64 [pairs][N][N]."""
+    _need(target, torch.float32, "target")
+    n = target.shape[-1]
+    b, e = sf_range if sf_range is not None else (0, n_sub)
+    out = torch.empty(((e - b + 1) // 2, n, n), dtype=torch.complex64, device=target.device)
+    lp, L = _lut_args(lut)
+    use_prng = prng_seed is not None
+    check(lib().holo_debug_ospr_pairs(target.data_ptr(), n, n_sub, lp, L, int(use_prng), prng_seed or 0, offset, b, e,
+                                      out.data_ptr(),
+                                      _stream(target.device)))
+    return out
+
 
 def launch_count() -> int:
     return int(lib().holo_launch_count())

@@ -139,7 +139,7 @@ struct PhaseRows {
     }
 };
 
-template <int N, int LMODE>
+template <int N, int LMODE, bool ZOUT = false>
 __global__ void __launch_bounds__(RowA<N>::WPC * 32)
 ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
                    int npairs, int last_pair_has_b, float2 *__restrict__ buf)
@@ -244,7 +244,8 @@ ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, c
 #pragma unroll
             for (int m = 0; m < E; ++m)
                 v[m] = sg[t + R1 * m];                       // conj(Z), built so by the producer
-            fft::fft2pass<N, false, 1, true>(v, sg, t, twr);
+            if constexpr (!ZOUT)                             // ZOUT: the test hook writes conj(Z) itself
+                fft::fft2pass<N, false, 1, true>(v, sg, t, twr);
             const int k = k0 + slot / 2;
             const int y = (slot & 1) ? (k > 0 ? N - k : N / 2) : k;
             float2 *o = buf + ((size_t)pair * N + y) * N;
@@ -271,7 +272,7 @@ struct RowA2 {
     static constexpr int UNITS_PER_PAIR = N / 2;
 };
 
-template <int N, int LMODE>
+template <int N, int LMODE, bool ZOUT = false>
 __global__ void __launch_bounds__(RowA2<N>::WPC * 32)
 ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
                     int npairs, int last_pair_has_b, float2 *__restrict__ buf)
@@ -361,7 +362,8 @@ ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = sg[t + R1 * m];                           // conj(Z), built so by the producer
-        fft::fft2pass<N, false, 1, true>(v, sg, t, twp);
+        if constexpr (!ZOUT)                                 // ZOUT: the test hook writes conj(Z) itself
+            fft::fft2pass<N, false, 1, true>(v, sg, t, twp);
         float2 *o = buf + ((size_t)pair * N + (h ? ym : y)) * N;
 #pragma unroll
         for (int m = 0; m < E; ++m)
@@ -810,6 +812,49 @@ holo_status finalize_frame(const float *acc, const float *T, int symmetrise, flo
                   symmetrise, scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse);
 }
 
+// Pass A over np sub-frame pairs starting at global sub-frame sf_first (ZOUT: the test hook
+// variant that stores conj(Z) instead of its row IFFT).
+template <int N, bool ZOUT>
+static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseSrc &ps, bool prng, uint64_t sf_first,
+                                 int np, int last_has_b, float2 *buf, cudaStream_t s)
+{
+    if constexpr (N >= 1024) {
+        using RA2 = RowA2<N>;
+        auto kern = prng                     ? ospr_rows_a2_kernel<N, LUT_PRNG, ZOUT>
+                  : ps.ix.mode == LUT_WRAP ? ospr_rows_a2_kernel<N, LUT_WRAP, ZOUT>
+                  : ps.ix.mode == LUT_POW2 ? ospr_rows_a2_kernel<N, LUT_POW2, ZOUT>
+                                           : ospr_rows_a2_kernel<N, LUT_GENERAL, ZOUT>;
+        const int grid = pipe_grid(kern, RA2::WPC * 32, RA2::SMEM, np * RA2::UNITS_PER_PAIR, RA2::UPC);
+        return launch(ZOUT ? K_RANDOMISE : K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA2::WPC * 32), RA2::SMEM, s, tw,
+                      Tf, ps, sf_first, np, last_has_b, buf);
+    } else {
+        using RA = RowA<N>;
+        auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG, ZOUT>
+                  : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP, ZOUT>
+                  : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2, ZOUT>
+                                           : ospr_rows_a_kernel<N, LUT_GENERAL, ZOUT>;
+        const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
+        return launch(ZOUT ? K_RANDOMISE : K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf,
+                      ps, sf_first, np, last_has_b, buf);
+    }
+}
+
+// The phase source of a call (host side).
+static holo_status make_phase_src(int n, const float2 *lut, uint64_t n_lut, bool prng, uint64_t seed,
+                                  uint64_t phase_offset, PhaseSrc *ps)
+{
+    const uint64_t P = (uint64_t)n * n;
+    ps->ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, n);
+    ps->lut = lut;                      // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
+    if (lut == nullptr && !prng)
+        HOLO_TRY(flat_lut(&ps->lut));
+    ps->off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
+    ps->p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
+    ps->seed = seed;
+    ps->off = phase_offset;
+    return HOLO_OK;
+}
+
 template <int N>
 static holo_status ospr_run(const float2 *tw, const float *target, int n_frames, int n_sub, const float2 *lut, uint64_t n_lut,
                             bool prng, uint64_t seed, uint64_t phase_offset, int sf_begin, int sf_end,
@@ -823,14 +868,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const int npairs_total = (nsh + 1) / 2;
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     PhaseSrc ps;
-    ps.ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
-    ps.lut = lut;                      // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
-    if (lut == nullptr && !prng)
-        HOLO_TRY(flat_lut(&ps.lut));
-    ps.off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
-    ps.p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
-    ps.seed = seed;
-    ps.off = phase_offset;
+    HOLO_TRY(make_phase_src(N, lut, n_lut, prng, seed, phase_offset, &ps));
     for (int f = 0; f < n_frames; ++f) {
         const float *Tf = target + (size_t)f * P;
         for (int c0 = 0; c0 < npairs_total; c0 += chunk) {
@@ -839,26 +877,8 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const int last_has_b = (last_sa + 1) < sf_end;
             uint8_t *bt = holo_bits ? w.bt + 2 * (size_t)c0 * (P / 8) : nullptr;
             {
-                using RA = RowA<N>;
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                if constexpr (N >= 1024) {
-                    using RA2 = RowA2<N>;
-                    auto kern = prng                     ? ospr_rows_a2_kernel<N, LUT_PRNG>
-                              : ps.ix.mode == LUT_WRAP ? ospr_rows_a2_kernel<N, LUT_WRAP>
-                              : ps.ix.mode == LUT_POW2 ? ospr_rows_a2_kernel<N, LUT_POW2>
-                                                       : ospr_rows_a2_kernel<N, LUT_GENERAL>;
-                    const int grid = pipe_grid(kern, RA2::WPC * 32, RA2::SMEM, np * RA2::UNITS_PER_PAIR, RA2::UPC);
-                    HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA2::WPC * 32), RA2::SMEM, s, tw, Tf, ps,
-                                    sf_first, np, last_has_b, w.buf));
-                } else {
-                    auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG>
-                              : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP>
-                              : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2>
-                                                       : ospr_rows_a_kernel<N, LUT_GENERAL>;
-                    const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
-                    HOLO_TRY(launch(K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf, ps,
-                                    sf_first, np, last_has_b, w.buf));
-                }
+                HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, prng, sf_first, np, last_has_b, w.buf, s)));
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
@@ -974,6 +994,45 @@ extern "C" holo_status holo_ospr_generate_prng(const float *target, int32_t n, i
 {
     return ospr_entry(target, n, n_frames, n_sub, nullptr, 0, true, seed, phase_offset, sf_begin, sf_end, holo_bits,
                       intensity, mse, omega, ws, ws_bytes, stream);
+}
+
+extern "C" holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int32_t n_sub, const holo_c64 *lut,
+                                             uint64_t n_lut, int32_t use_prng, uint64_t prng_seed,
+                                             uint64_t phase_offset, int32_t sf_begin, int32_t sf_end,
+                                             holo_c64 *z_out, holo_stream stream)
+{
+    HOLO_TRY(check_n(n));
+    HOLO_CHECK_ARG(target != nullptr && z_out != nullptr, "target/z_out is NULL");
+    HOLO_CHECK_ARG(n_sub >= 1 && 0 <= sf_begin && sf_begin < sf_end && sf_end <= n_sub,
+                   "sub-frame range [%d,%d) must be a non-empty part of [0,%d)", sf_begin, sf_end, n_sub);
+    HOLO_CHECK_ARG(n_lut < (1ull << 31), "n_lut must be < 2^31");
+    HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
+    HOLO_CHECK_ARG(!use_prng || lut == nullptr, "use_prng excludes a LUT");
+    const float2 *tw = nullptr;
+    HOLO_TRY(fft::twiddles(&tw));
+    const bool prng = use_prng != 0;
+    PhaseSrc ps;
+    HOLO_TRY(make_phase_src(n, (const float2 *)lut, n_lut, prng, prng_seed, phase_offset, &ps));
+    const int npairs = (sf_end - sf_begin + 1) / 2;
+    const int last_has_b = (sf_begin + 2 * (npairs - 1) + 1) < sf_end;
+    cudaStream_t s = (cudaStream_t)stream;
+    float2 *z = (float2 *)z_out;
+#define HOLO_PAIRS_CASE(NN)                                                                                  \
+    case NN:                                                                                                 \
+        return launch_pass_a<NN, true>(tw, target, ps, prng, (uint64_t)sf_begin, npairs, last_has_b, z, s);
+    switch (n) {
+        HOLO_PAIRS_CASE(16)
+        HOLO_PAIRS_CASE(32)
+        HOLO_PAIRS_CASE(64)
+        HOLO_PAIRS_CASE(128)
+        HOLO_PAIRS_CASE(256)
+        HOLO_PAIRS_CASE(512)
+        HOLO_PAIRS_CASE(1024)
+        HOLO_PAIRS_CASE(2048)
+    default:
+        return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
+    }
+#undef HOLO_PAIRS_CASE
 }
 
 extern "C" holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, int32_t n,

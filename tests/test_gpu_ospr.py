@@ -48,6 +48,55 @@ def test_randomise_bit_exact(L, offset):
     assert np.array_equal(R.view(np.uint32), ref.view(np.uint32))
 
 
+# ---- pass A's production producer (a1, a2 + Hermitian pairing) ----------------------------------------
+
+def _mirror(R):
+    """R(-p): (y, x) -> ((-y) mod N, (-x) mod N)."""
+    return np.roll(np.flip(R, (0, 1)), 1, (0, 1))
+
+
+@pytest.mark.parametrize("n,S,L,offset,rng", [
+    (64, 5, 4096, 0, (0, 5)),              # LUT_WRAP fast path (no wrap), odd tail
+    (64, 4, 1021, 77, (1, 4)),             # LUT_GENERAL, shard with an odd last pair
+    (128, 3, 1 << 12, 3 * 128 + 5, (0, 3)),   # LUT_POW2 (L a power of two), unaligned offset
+    (128, 2, 0, 0, (0, 2)),                # L = 0: the flat pool
+    (256, 2, 100003, (1 << 33) + 9, (0, 2)),  # offset beyond 2^32
+    (1024, 3, 65536, 0, (0, 3)),           # the C3 pool (rows_a2 kernel)
+    (1024, 2, 1009, 12345, (0, 2)),        # rows_a2, LUT_GENERAL
+    (2048, 1, 7, 3, (0, 1)),               # rows_a2, tiny LUT, unpaired
+])
+def test_pass_a_pairs_match_oracle(n, S, L, offset, rng):
+    """The randomisation pass A feeds the row IFFT: conj(Z) with Z = H_a + i H_b,
+    H_s = R_s + conj(R_s(-p)) and R_s = oracle.apply_phase at cursor offset + s N^2 (R-7,
+    DESIGN.md §5). fp32: each component is a sum of two products |t c| <= 1, so every
+    element is within 2 ulp(4)."""
+    T = blobs_target(41 + n + S, n, 6, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n))
+    lg, lo = lut_pair(LUT_SEED + 3, L)
+    b, e = rng
+    Z = to_np(hb.debug_ospr_pairs(cuda_target(T), S, lg, offset, (b, e)))
+    P = n * n
+    for j, s in enumerate(range(b, e, 2)):
+        Ra = oracle.apply_phase(T, lo, offset + s * P)
+        Rb = oracle.apply_phase(T, lo, offset + (s + 1) * P) if s + 1 < e else np.zeros_like(Ra)
+        ref = np.conj((Ra + np.conj(_mirror(Ra))) + 1j * (Rb + np.conj(_mirror(Rb))))
+        assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, s)
+
+
+@pytest.mark.parametrize("n,offset", [(64, 0), (1024, (1 << 35) + 17)])
+def test_pass_a_pairs_prng_match_oracle(n, offset):
+    """The same with the on-the-fly source (R-5 phases of SplitMix64 draws; recipe
+    computed in fp64 on both sides, so R matches apply_phase_prng to fp32 rounding)."""
+    T = blobs_target(77 + n, n, 6, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n))
+    S, seed = 3, 2004
+    Z = to_np(hb.debug_ospr_pairs(cuda_target(T), S, None, offset, (0, S), prng_seed=seed))
+    P = n * n
+    for j, s in enumerate(range(0, S, 2)):
+        Ra = oracle.apply_phase_prng(T, seed, offset + s * P)
+        Rb = oracle.apply_phase_prng(T, seed, offset + (s + 1) * P) if s + 1 < S else np.zeros_like(Ra)
+        ref = np.conj((Ra + np.conj(_mirror(Ra))) + 1j * (Rb + np.conj(_mirror(Rb))))
+        assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, s)
+
+
 # ---- unitary DFT hook ------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048])
