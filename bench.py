@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -172,6 +173,20 @@ def timed_loop(step_fn, k, w, world, flush):
     return total, per
 
 
+HBM_SPEC_GBS = 8000.0   # B200 datasheet HBM3e bandwidth (report both denominators)
+
+
+def fft_rate(units_per_s, P, paired):
+    """FFT GFLOP/s at 5 P log2 P flop per 2D transform of P points (BASELINE north_star's
+    count), two transforms (back- and forward-propagation) per unit.  `nominal` counts every
+    unit's own transforms; `executed` the transforms actually run (Hermitian pairing packs two
+    OSPR sub-frames into one complex transform)."""
+    per_unit = 2 * 5 * P * math.log2(P)
+    nominal = units_per_s * per_unit / 1e9
+    return {"unit": "GFLOP/s", "nominal": nominal, "executed": nominal / 2 if paired else nominal,
+            "flop_per_unit_nominal": per_unit, "count": "5 P log2 P per 2D DFT of P points, 2 per unit"}
+
+
 def graphed(step_fn, enabled):
     """Capture one step (after it has run eagerly once, so every one-off host set-up --
     twiddle tables, shared-memory opt-ins -- is done) into a CUDA graph and return its
@@ -251,6 +266,14 @@ def graphed_stages(pre, collective, post, enabled):
     collective()
     post()
     torch.cuda.synchronize()
+    if getattr(collective, "local", False):   # no exchange (one rank): one graph for the whole step
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            pre()
+            collective()
+            post()
+        torch.cuda.synchronize()
+        return g.replay
     g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(g1):
         pre()
@@ -377,7 +400,9 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": kern[dom]["avg_us"],
-                     "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                     "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                     "peak_spec": HBM_SPEC_GBS, "frac_spec": achieved / HBM_SPEC_GBS},
+        "fft": fft_rate(S * args.steps / (total_ms / 1e3), P, paired=True),
         "kernels": kern,
         "clocks": clk.summary(),
         "device": {"name": props.name, "sms": props.multi_processor_count,
@@ -473,7 +498,9 @@ def run_gpu(args):
                        "launch": "CUDA graph replay" if use_graph else "eager launches"},
             "roofline": {"bound": "hbm", "kernel": gdom, "achieved": gach, "peak": hbm_peak, "unit": "GB/s",
                          "frac": gach / hbm_peak, "algorithmic_bytes_per_launch": gbytes[gdom],
-                         "avg_launch_us": gk[gdom]["avg_us"]},
+                         "avg_launch_us": gk[gdom]["avg_us"], "peak_spec": HBM_SPEC_GBS,
+                         "frac_spec": gach / HBM_SPEC_GBS},
+            "fft": fft_rate(B * iters * ks / (gm / 1e3), P4, paired=False),
             "kernels": gk,
         }
 

@@ -137,6 +137,15 @@ holo_status ensure_smem(const void *fn, size_t smem)
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     if (e != cudaSuccess)
         return cuda_status(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    static const int carveout = [] {   // HOLO_CARVEOUT=percent: shared-memory share of L1 (experiments)
+        const char *c = getenv("HOLO_CARVEOUT");
+        return c ? atoi(c) : -1;
+    }();
+    if (carveout >= 0) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+        if (e != cudaSuccess)
+            return cuda_status(e, "cudaFuncSetAttribute(PreferredSharedMemoryCarveout)");
+    }
     g_smem_done.insert(key);
     return HOLO_OK;
 }

@@ -74,7 +74,10 @@ class ShardedOspr:
                 out.mse = mse_out
                 self.generate(target, n_sub, lut, phase_offset=phase_offset, omega=omega, workspace=workspace,
                               out=out)
-            return whole, (lambda: None), (lambda: None)
+            def no_exchange():
+                pass
+            no_exchange.local = True                 # marks a collective with nothing to exchange
+            return whole, no_exchange, (lambda: None)
 
         def pre():
             self.generate(target, n_sub, lut, phase_offset=phase_offset, sf_range=(b, e), want_mse=False,
@@ -83,6 +86,7 @@ class ShardedOspr:
         def collective():
             if self.world > 1:
                 self.all_reduce(out.intensity)
+        collective.local = False
 
         def post():
             self.finalize(target, out.intensity, n_sub, omega=omega, out=out.intensity, mse_out=mse_out,
