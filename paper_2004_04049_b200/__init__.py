@@ -9,5 +9,6 @@ missing.
 from .api import *  # noqa: F401,F403
 from .api import __all__ as _api_all
 from ._lib import HoloError, lib  # noqa: F401
+from .stream import OsprStream  # noqa: F401
 
-__all__ = list(_api_all) + ["HoloError", "lib"]
+__all__ = list(_api_all) + ["HoloError", "lib", "OsprStream"]

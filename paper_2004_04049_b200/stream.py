@@ -1,0 +1,119 @@
+"""Pipelined OSPR frame stream: SURVEY.md §8(f) f3, the "packed-frame output stream for a binary
+display at video rate" (the 1024x1024 ferroelectric SLM demonstration).
+
+A display shows frame set f as N_SF binary sub-frames (Fig. 2 right); frame set f + 1 uses
+the continuing phase cursor, off0 + (f + 1) N_SF N^2 (reading R-2).  The stream takes each
+frame set's target amplitude from pinned host memory and returns its packed sub-frame holograms
+(R-8 layout, [N_SF][N][N/8] bytes) and its MSE (R-12) to pinned host memory.  Three CUDA streams
+overlap the steps of consecutive frame sets:
+
+    h2d  : target f + 1  host -> device            (copy engine)
+    comp : [a0,] ospr_generate of frame set f        (libholo kernels)
+    d2h  : holograms + MSE of f - 1  device -> host  (copy engine)
+
+with `depth` device slots for the per-frame buffers (targets and outputs) and one workspace (the
+compute steps of consecutive frame sets run in order on `comp`).  Cross-stream order comes from
+CUDA events only; the host never blocks in submit().  Every kernel is libholo's: this module is
+plumbing (PyTorch streams, events and pinned memory).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence, Tuple
+
+import torch
+
+from .api import OsprResult, default_omega, ospr_generate, ospr_workspace_bytes
+
+
+class OsprStream:
+    """Frame-set pipeline over one GPU.
+
+    submit(target_host) enqueues frame set f (returns f); result(f) waits for its outputs and
+    returns host views (bits [N_SF][N][N/8] uint8, mse float64 [1], intensity [N][N] float32 or
+    None) that stay valid until frame set f + depth is submitted.  The caller keeps target_host
+    unchanged until done(f) (or any later result) reports the frame set's copy complete.
+    """
+
+    def __init__(self, n: int, n_sub: int, lut: Optional[torch.Tensor] = None, *, depth: int = 3,
+                 phase_offset: int = 0, advance: bool = True, omega: Optional[Sequence[int]] = None,
+                 want_intensity: bool = False, before_each: Optional[Callable[[], None]] = None,
+                 device: Optional[torch.device] = None):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.n_sub, self.lut, self.depth = n, n_sub, lut, depth
+        self.off0, self.advance = phase_offset, advance
+        self.omega = tuple(omega) if omega is not None else default_omega(n, "ospr")
+        self.before_each = before_each
+        self.dev = dev
+        self.h2d = torch.cuda.Stream(dev)
+        self.comp = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.ws = torch.empty(ospr_workspace_bytes(n, 1, n_sub), dtype=torch.uint8, device=dev)
+        f32, u8, f64 = torch.float32, torch.uint8, torch.float64
+        self.t_dev = [torch.empty((1, n, n), dtype=f32, device=dev) for _ in range(depth)]
+        self.out = [OsprResult(bits=torch.empty((1, n_sub, n, n // 8), dtype=u8, device=dev),
+                               intensity=torch.empty((1, n, n), dtype=f32, device=dev),
+                               mse=torch.empty(1, dtype=f64, device=dev)) for _ in range(depth)]
+        self.bits_host = [torch.empty((n_sub, n, n // 8), dtype=u8).pin_memory() for _ in range(depth)]
+        self.mse_host = [torch.empty(1, dtype=f64).pin_memory() for _ in range(depth)]
+        self.inten_host = [torch.empty((n, n), dtype=f32).pin_memory() for _ in range(depth)] \
+            if want_intensity else None
+        ev = lambda: [torch.cuda.Event() for _ in range(depth)]   # noqa: E731
+        self.h2d_done, self.comp_done, self.d2h_done = ev(), ev(), ev()
+        self.used = [False] * depth
+        self.f = 0
+
+    def frame_offset(self, f: int) -> int:
+        """Phase cursor of frame set f (R-2: off0 + f N_SF N^2 when advancing)."""
+        return self.off0 + (f * self.n_sub * self.n * self.n if self.advance else 0)
+
+    def submit(self, target_host: torch.Tensor) -> int:
+        if target_host.dtype != torch.float32 or tuple(target_host.shape[-2:]) != (self.n, self.n):
+            raise ValueError(f"target_host must be float32 [{self.n}][{self.n}]")
+        f = self.f
+        s = f % self.depth
+        if self.used[s]:
+            # slot reuse: the previous frame set of this slot must have read its target (comp)
+            # and shipped its outputs (d2h) before they are overwritten
+            self.h2d.wait_event(self.comp_done[s])
+            self.comp.wait_event(self.d2h_done[s])
+        with torch.cuda.stream(self.h2d):
+            self.t_dev[s][0].copy_(target_host, non_blocking=True)
+            self.h2d_done[s].record(self.h2d)
+        self.comp.wait_event(self.h2d_done[s])
+        with torch.cuda.stream(self.comp):
+            if self.before_each is not None:
+                self.before_each()
+            ospr_generate(self.t_dev[s], self.n_sub, self.lut, phase_offset=self.frame_offset(f),
+                          omega=self.omega, workspace=self.ws, out=self.out[s])
+            self.comp_done[s].record(self.comp)
+        self.d2h.wait_event(self.comp_done[s])
+        with torch.cuda.stream(self.d2h):
+            o = self.out[s]
+            self.bits_host[s].copy_(o.bits[0], non_blocking=True)
+            self.mse_host[s].copy_(o.mse, non_blocking=True)
+            if self.inten_host is not None:
+                self.inten_host[s].copy_(o.intensity[0], non_blocking=True)
+            self.d2h_done[s].record(self.d2h)
+        self.used[s] = True
+        self.f = f + 1
+        return f
+
+    def _slot(self, f: int) -> int:
+        if not (self.f - self.depth <= f < self.f):
+            raise ValueError(f"frame set {f} is not among the last {self.depth} submitted")
+        return f % self.depth
+
+    def done(self, f: int) -> bool:
+        """True once frame set f's outputs are in host memory (its target copy is complete too)."""
+        return self.d2h_done[self._slot(f)].query()
+
+    def result(self, f: int) -> Tuple[torch.Tensor, torch.Tensor, Optional[torch.Tensor]]:
+        s = self._slot(f)
+        self.d2h_done[s].synchronize()
+        return self.bits_host[s], self.mse_host[s], (self.inten_host[s] if self.inten_host is not None else None)
+
+    def drain(self) -> None:
+        """Block until every submitted frame set is complete."""
+        self.d2h.synchronize()
