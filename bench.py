@@ -148,29 +148,31 @@ def max_over_ranks(x, world):
 
 
 def timed_loop(step_fn, k, w, world, flush):
-    """W warm-up steps, then K timed steps, each: flush L2, barrier + sync, events."""
+    """W warm-up steps, then K timed steps bracketed as a block by a barrier + device sync on
+    both sides.  Inside the block each step is: L2 flush, event, step, event, all enqueued
+    on the stream without a host sync, so the host queues step i+1 while the device runs
+    step i.  The step time is the sum of the per-step event intervals: device time of the
+    steps alone, the flushes between them excluded."""
     import torch
     for _ in range(w):
         step_fn()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
-    total = 0.0
-    per = []
+    barrier(world)
+    torch.cuda.synchronize()
+    evs = []
     for _ in range(k):
         flush()
-        barrier(world)
-        torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s)
         step_fn()
         b.record(s)
-        torch.cuda.synchronize()
-        barrier(world)
-        ms = a.elapsed_time(b)
-        per.append(ms)
-        total += ms
-    return total, per
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    barrier(world)
+    per = [a.elapsed_time(b) for a, b in evs]
+    return sum(per), per
 
 
 HBM_SPEC_GBS = 8000.0   # B200 datasheet HBM3e bandwidth (SURVEY.md §8(d): report both denominators)
@@ -349,6 +351,18 @@ def run_gpu(args):
     launches_per_step = hb.launch_count() - l0                 # libholo kernels in one step
     timed_step = graphed_stages(*ospr_stages(args.lut, lut_buf), use_graph)
     with Clocks(local) as clk:
+        # the timed block lasts milliseconds; the sampler (100 ms period) sees the clocks of the
+        # same step running untimed for 0.6 s right before it (extra warm-up, same load)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            flush()
+            timed_step()
+        torch.cuda.synchronize()
+        n_load = min(20000, int(max_over_ranks(math.ceil(0.6 / max((time.perf_counter() - t0) / 5, 1e-5)), world)))
+        for _ in range(n_load):      # the same count on every rank (the step may hold a collective)
+            flush()
+            timed_step()
+        torch.cuda.synchronize()
         total_ms, per = timed_loop(timed_step, args.steps, args.warmup, world, flush)
     launches_timed = launches_per_step * args.steps
     total_ms = max_over_ranks(total_ms, world)
