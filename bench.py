@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["holo", "reference"], default="holo")
     ap.add_argument("--lut", type=int, default=1 << 16, help="headline LUT length")
+    ap.add_argument("--ospr-shard", choices=["frames", "subframes"], default="frames",
+                    help="N > 1: each rank its own C3 frame set (weak, no collective; default) or one frame "
+                         "set's sub-frames split across ranks + NCCL all-reduce of the intensity (strong)")
     ap.add_argument("--no-gs", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -311,24 +314,30 @@ def run_gpu(args):
     # HOLO_BENCH_FAKE_WORLD=k (testing only, N = 1): run rank 0's shard of a k-way split with a
     # no-op collective, to exercise the N > 1 step structure (graphs around the collective)
     fake = int(os.environ.get("HOLO_BENCH_FAKE_WORLD", "0")) if world == 1 else 0
-    sworld = fake if fake > 1 else world
-    sb, se = shard_range(S, sworld, rank)
+    mode = "subframes" if fake > 1 else args.ospr_shard
+    # frames: rank r runs global frame set r (cursor off0 + r N_SF P, R-2), independent of the
+    # others -- no collective; subframes: one frame set's sub-frames split over the ranks, C-1
+    frames_mode = (mode == "frames")
+    sworld = 1 if frames_mode else (fake if fake > 1 else world)
+    srank = 0 if frames_mode else rank
+    frame_off = rank * S * P if frames_mode else 0
+    sb, se = shard_range(S, sworld, srank)
     full = (sworld == 1)
     ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device=dev)
     lut_buf = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
     out = hb.OsprResult(bits=torch.empty((1, se - sb, n, n // 8), dtype=torch.uint8, device=dev),
                         intensity=torch.empty((1, n, n), dtype=torch.float32, device=dev),
                         mse=torch.empty(1, dtype=torch.float64, device=dev) if full else None)
-    mean_buf = torch.empty((1, n, n), dtype=torch.float32, device=dev)
     mse_buf = torch.empty(1, dtype=torch.float64, device=dev)
 
     from paper_2004_04049_b200.parallel import ShardedOspr
-    sharded = ShardedOspr(sworld, rank, all_reduce=(lambda t: None)) if fake > 1 else ShardedOspr(world, rank)
+    sharded = ShardedOspr(sworld, srank, all_reduce=(lambda t: None)) if fake > 1 else ShardedOspr(sworld, srank)
 
     def ospr_stages(L, lut, T_in=None):
         """(pre, C-1, post) of one OSPR step: a0 + this rank's shard, the all-reduce of the
-        partial intensity (N > 1), then mean + MSE (a7)."""
-        pre, coll, post = sharded.stages(T if T_in is None else T_in, S, lut[:L], ws, out, mse_buf)
+        partial intensity (sub-frame shards over N > 1 ranks), then mean + MSE (a7)."""
+        pre, coll, post = sharded.stages(T if T_in is None else T_in, S, lut[:L], ws, out, mse_buf,
+                                         phase_offset=frame_off)
 
         def pre_a0():
             hb.lut_generate(LUT_SEED, L, out=lut[:L])                               # a0
@@ -367,11 +376,12 @@ def run_gpu(args):
     launches_timed = launches_per_step * args.steps
     total_ms = max_over_ranks(total_ms, world)
     ms_step = total_ms / args.steps
-    value = S * args.steps / (total_ms / 1e3)
+    sets_per_step = world if frames_mode else 1               # frame sets all ranks finish per step
+    value = sets_per_step * S * args.steps / (total_ms / 1e3)
 
     # per-kernel device time: the same step in the same launch configuration, every kernel
     # bracketed by CUDA events on its launch stream, K more steps after an L2 flush each
-    kern = kernel_times(hb, step, args.steps, flush, use_graph and world == 1)   # (no NCCL in a graph)
+    kern = kernel_times(hb, step, args.steps, flush, use_graph and sworld == 1)   # (no NCCL in a graph)
     step_kernel_ms = sum(v["total_ms"] for v in kern.values()) / args.steps
 
     # roofline of the dominant kernel (algorithmic bytes per launch)
@@ -401,27 +411,51 @@ def run_gpu(args):
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak" if frames_mode else "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Gaussian-blob targets, holo_synth; stands in for USC-SIPI images)",
-        "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step (a0 LUT build + "
-                               "a1-a7 incl. MSE); BASELINE configs[2]",
+        "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step and GPU (a0 LUT "
+                               "build + a1-a7 incl. MSE); BASELINE configs[2]",
                    "n": n, "n_sub": S, "lut_len": args.lut, "lut_seed": LUT_SEED,
                    "l2": "flushed before every timed step (256 MiB write)",
-                   "launch": ("CUDA graph replay of the step (captured once)" if world == 1 else
+                   "launch": ("CUDA graph replay of the step (captured once)" if sworld == 1 else
                               "CUDA graph replays around the eager NCCL all-reduce") if use_graph else "eager launches",
-                   "parallelism": f"sub-frame shards x{world}" + (" + NCCL all-reduce of intensity" if world > 1 else "")},
+                   "parallelism": (f"frame-set shards x{world}: rank r runs global frame set r (cursor off0 + "
+                                   "r*N_SF*N^2), no collective" if frames_mode else
+                                   f"sub-frame shards x{sworld} + NCCL all-reduce of the intensity")},
         "gpu_launches": launches_timed,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": kern[dom]["avg_us"],
                      "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                      "peak_spec": HBM_SPEC_GBS, "frac_spec": achieved / HBM_SPEC_GBS},
-        "fft": fft_rate(S * args.steps / (total_ms / 1e3), P, paired=True),
+        "fft": fft_rate(value, P, paired=True),
         "kernels": kern,
         "clocks": clk.summary(),
         "device": {"name": props.name, "sms": props.multi_processor_count,
                    "l2_mb": getattr(props, "L2_cache_size", 0) / 2 ** 20},
     }
+
+    # ---------------- N > 1: one frame set split over the ranks (C-1 over NCCL) ----------------
+    if world > 1 and frames_mode and world <= S:       # every rank holds sub-frames (same collectives)
+        ssb, sse = shard_range(S, world, rank)
+        sh = ShardedOspr(world, rank)
+        s_out = hb.OsprResult(bits=torch.empty((1, sse - ssb, n, n // 8), dtype=torch.uint8, device=dev),
+                              intensity=torch.empty((1, n, n), dtype=torch.float32, device=dev), mse=None)
+        s_mse = torch.empty(1, dtype=torch.float64, device=dev)
+        pre, coll, post = sh.stages(T, S, lut_buf[:args.lut], ws, s_out, s_mse)
+
+        def s_pre():
+            hb.lut_generate(LUT_SEED, args.lut, out=lut_buf[:args.lut])
+            pre()
+        sst = graphed_stages(s_pre, coll, post, use_graph)
+        stm, _ = timed_loop(sst, args.steps, args.warmup, world, flush)
+        stm = max_over_ranks(stm, world)
+        result["subframe_shards"] = {
+            "value": S * args.steps / (stm / 1e3), "unit": UNIT, "ms_per_step": stm / args.steps,
+            "scaling": "strong", "mse": float(s_mse.item()),
+            "what": f"one C3 frame set per step, its {S} sub-frames split over {world} ranks "
+                    "(shard_range), NCCL all-reduce of the partial intensity, then mean + MSE on every rank "
+                    "(BASELINE configs[4]'s partition; graphs around the eager all-reduce)"}
 
     # ---------------- LUT sweep of C3 ----------------
     if not args.no_sweep and world == 1:
@@ -446,17 +480,19 @@ def run_gpu(args):
         del big
 
     # ---------------- e2e through the public API with host buffers ----------------
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and frames_mode:
         # the frame stream: pinned host target -> H2D -> a0 + ospr_generate ->
-        # D2H of the packed holograms and MSE, per frame set, pipelined over three CUDA streams
+        # D2H of the packed holograms and MSE, per frame set, pipelined over three CUDA streams;
+        # rank r streams global frame sets r, r + N, r + 2N, ...
         hosts = [torch.from_numpy(target_for(w3)).pin_memory() for _ in range(3)]
         lut_e2e = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
-        stream = hb.OsprStream(n, S, lut_e2e[:args.lut], depth=3,
+        stream = hb.OsprStream(n, S, lut_e2e[:args.lut], depth=3, phase_offset=rank * S * P, frame_stride=world,
                                before_each=lambda: hb.lut_generate(LUT_SEED, args.lut, out=lut_e2e[:args.lut]))
         for i in range(args.warmup):
             stream.submit(hosts[i % 3])
         stream.drain()
         torch.cuda.synchronize()
+        barrier(world)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream.h2d)
         first = stream.f
@@ -464,11 +500,13 @@ def run_gpu(args):
             stream.submit(hosts[i % 3])
         b.record(stream.d2h)
         torch.cuda.synchronize()
-        tm = a.elapsed_time(b)
+        barrier(world)
+        tm = max_over_ranks(a.elapsed_time(b), world)
         mse_e2e = float(stream.result(stream.f - 1)[1][0])
-        result["e2e"] = {"value": S * args.steps / (tm / 1e3), "unit": UNIT,
-                         "h2d_bytes_per_step": hosts[0].numel() * 4,
-                         "d2h_bytes_per_step": stream.bits_host[0].numel() + 8,
+        result["e2e"] = {"value": world * S * args.steps / (tm / 1e3), "unit": UNIT,
+                         "h2d_bytes_per_step": world * hosts[0].numel() * 4,
+                         "d2h_bytes_per_step": world * (stream.bits_host[0].numel() + 8),
+                         "bytes_per_step": "all ranks (one frame set per rank per step)",
                          "ms_per_step": tm / args.steps, "frame_sets": [first, stream.f], "mse_last": mse_e2e,
                          "what": "paper_2004_04049_b200.OsprStream (public API): per frame set a pinned host target "
                                  "-> device, a0 LUT build, ospr_generate (a1-a7) with the continuing cursor, packed "

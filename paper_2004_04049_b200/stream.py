@@ -35,14 +35,15 @@ class OsprStream:
     """
 
     def __init__(self, n: int, n_sub: int, lut: Optional[torch.Tensor] = None, *, depth: int = 3,
-                 phase_offset: int = 0, advance: bool = True, omega: Optional[Sequence[int]] = None,
+                 phase_offset: int = 0, advance: bool = True, frame_stride: int = 1,
+                 omega: Optional[Sequence[int]] = None,
                  want_intensity: bool = False, before_each: Optional[Callable[[], None]] = None,
                  device: Optional[torch.device] = None):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.n, self.n_sub, self.lut, self.depth = n, n_sub, lut, depth
-        self.off0, self.advance = phase_offset, advance
+        self.off0, self.advance, self.frame_stride = phase_offset, advance, frame_stride
         self.omega = tuple(omega) if omega is not None else default_omega(n, "ospr")
         self.before_each = before_each
         self.dev = dev
@@ -65,8 +66,10 @@ class OsprStream:
         self.f = 0
 
     def frame_offset(self, f: int) -> int:
-        """Phase cursor of frame set f (R-2: off0 + f N_SF N^2 when advancing)."""
-        return self.off0 + (f * self.n_sub * self.n * self.n if self.advance else 0)
+        """Phase cursor of this stream's frame set f: off0 + f * frame_stride * N_SF N^2 when
+        advancing (R-2).  frame_stride = k with off0 = r N_SF N^2 gives stream r of k the global
+        frame sets r, r + k, r + 2k, ... (one stream per GPU)."""
+        return self.off0 + (f * self.frame_stride * self.n_sub * self.n * self.n if self.advance else 0)
 
     def submit(self, target_host: torch.Tensor) -> int:
         if target_host.dtype != torch.float32 or tuple(target_host.shape[-2:]) != (self.n, self.n):

@@ -19,19 +19,21 @@ def targets(n, k, seed):
     return [blobs_target(seed + i, n, 6, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n)) for i in range(k)]
 
 
-@pytest.mark.parametrize("n,S,L,depth,advance", [
-    (256, 6, 1021, 3, True),
-    (256, 5, 1021, 2, True),       # odd N_SF: unpaired last sub-frame
-    (128, 4, 4096, 1, True),       # depth 1: fully serialised
-    (256, 6, 1021, 3, False),      # every frame set at off0
-    (1024, 24, 1 << 16, 3, True),  # C3
+@pytest.mark.parametrize("n,S,L,depth,advance,stride", [
+    (256, 6, 1021, 3, True, 1),
+    (256, 5, 1021, 2, True, 1),       # odd N_SF: unpaired last sub-frame
+    (128, 4, 4096, 1, True, 1),       # depth 1: fully serialised
+    (256, 6, 1021, 3, False, 1),      # every frame set at off0
+    (256, 6, 1021, 3, True, 4),       # stream 0 of 4 (one per GPU): global frame sets 0, 4, 8, ...
+    (1024, 24, 1 << 16, 3, True, 1),  # C3
 ])
-def test_stream_matches_direct_calls(n, S, L, depth, advance):
+def test_stream_matches_direct_calls(n, S, L, depth, advance, stride):
     off0 = 12345
     lg, _ = lut_pair(LUT_SEED, L)
     Ts = targets(n, 7, 600 + n)
     hosts = [torch.from_numpy(T).pin_memory() for T in Ts]
-    st = hb.OsprStream(n, S, lg, depth=depth, phase_offset=off0, advance=advance, want_intensity=True)
+    st = hb.OsprStream(n, S, lg, depth=depth, phase_offset=off0, advance=advance, frame_stride=stride,
+                       want_intensity=True)
     got = []
     for f, h in enumerate(hosts):
         st.submit(h)
@@ -46,7 +48,7 @@ def test_stream_matches_direct_calls(n, S, L, depth, advance):
     assert [g for g, *_ in got] == list(range(len(hosts)))
     P = n * n
     for g, b, m, i in got:
-        ref = hb.ospr_generate(cuda_target(Ts[g]), S, lg, phase_offset=off0 + (g * S * P if advance else 0))
+        ref = hb.ospr_generate(cuda_target(Ts[g]), S, lg, phase_offset=off0 + (g * stride * S * P if advance else 0))
         torch.cuda.synchronize()
         assert torch.equal(b, ref.bits[0].cpu()), g
         assert torch.equal(m, ref.mse.cpu()), g
