@@ -385,10 +385,16 @@ __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
     return x ^ t ^ (t << 28);
 }
 
+// Columns per OSPR column-pass tile (see OsprColBody::kWidth); host and device agree on it.
+constexpr int ospr_col_width(int n) { return n >= 2048 ? 4 : 8; }
+
 template <int N>
 struct OsprColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
-    static constexpr int kWidth = 8;   // columns per tile
+    // columns per tile: 8 (one packed byte per tile row); N = 2048: 4 (a nibble per tile row),
+    // so that three 2048-row stages fit in shared memory and the ring overlaps load, transform
+    // and store (an 8-column tile leaves room for one stage only)
+    static constexpr int kWidth = ospr_col_width(N);
     struct Args {
         const float2 *tw;
         float2 *buf;
@@ -402,7 +408,8 @@ struct OsprColBody {
     {
         constexpr int R1 = F::T, E = F::E;   // element m of thread t = row t + R1*m; W columns per tile
         const bool has_b = (pair < a.npairs - 1) || a.last_has_b;
-        static_assert(E <= 64 && W == 8, "bit words hold at most 64 rows per thread; one byte per tile row");
+        static_assert(E <= 64 && (W == 8 || W == 4), "bit words hold at most 64 rows per thread; a byte or "
+                                                       "nibble per tile row");
         using Word = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
         static_assert(2 * W * R1 * sizeof(Word) <= ColPipe<N, 0, W>::SCRATCH_BYTES, "scratch holds both bit planes");
         Word *sw = reinterpret_cast<Word *>(scratch);            // [frame 2][t R1][c W] sign words
@@ -447,8 +454,8 @@ struct OsprColBody {
                 const int f = task / (R1 * RG), rem = task % (R1 * RG), tt = rem % R1, rb = rem / R1;
                 if (f == 1 && !has_b)
                     continue;
-                Word q[W];                                       // the 8 words, vector loads
-                if constexpr (sizeof(Word) == 4) {
+                Word q[W];                                       // the W words, vector loads
+                if constexpr (sizeof(Word) == 4 && W == 8) {
                     const uint4 *q4 = reinterpret_cast<const uint4 *>(sw + (f * R1 + tt) * W);
                     const uint4 lo = q4[0], hi = q4[1];
                     q[0] = lo.x, q[1] = lo.y, q[2] = lo.z, q[3] = lo.w, q[4] = hi.x, q[5] = hi.y, q[6] = hi.z, q[7] = hi.w;
@@ -462,7 +469,8 @@ struct OsprColBody {
                 for (int cc = 0; cc < W; ++cc)
                     m |= (uint64_t)((q[cc] >> (8 * rb)) & 0xFFu) << (8 * (7 - cc));
                 m = transpose8x8(m);
-                uint8_t *dst = a.bits + ((size_t)(2 * pair + f) * (N / 8) + ct) * N + tt + R1 * 8 * rb;
+                // W = 4: the byte's high nibble holds the tile's 4 columns (MSB-first), the low one 0
+                uint8_t *dst = a.bits + ((size_t)(2 * pair + f) * (N / W) + ct) * N + tt + R1 * 8 * rb;
 #pragma unroll
                 for (int r = 0; r < RPG; ++r)
                     dst[r * R1] = (uint8_t)(m >> (8 * r));
@@ -478,6 +486,8 @@ struct OsprColBody {
 template <int N>
 struct BitsT {
     static constexpr int C = N / 8, YB = N < 32 ? N : 32, BLOCKS_PER_Q = N / YB;
+    static constexpr int W = OsprColBody<N>::kWidth;   // staging: one byte (W = 8) or nibble (W = 4) per tile row
+    static constexpr size_t BYTES_PER_SUBFRAME = (size_t)N * (N / W);
 };
 
 template <int N, int NT = 256>
@@ -487,7 +497,8 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
     constexpr int C = BitsT<N>::C, YB = BitsT<N>::YB;
     __shared__ __align__(16) uint8_t sm[C][YB + 4];
     const int y0 = yblk * YB;
-    const uint8_t *src = bt + (size_t)q * C * N + y0;
+    constexpr int TW = BitsT<N>::W;
+    const uint8_t *src = bt + (size_t)q * BitsT<N>::BYTES_PER_SUBFRAME + y0;
     uint8_t *dst = out + ((size_t)q * N + y0) * C;
     if constexpr (N >= 32) {
         constexpr int WPR = YB / 4, WORDS = C * WPR, PER = (WORDS + NT - 1) / NT;   // words per ct row
@@ -495,7 +506,17 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int i = threadIdx.x + NT * j;
-            w[j] = i < WORDS ? __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(i / WPR) * N) + i % WPR) : 0u;
+            if constexpr (TW == 8) {
+                w[j] = i < WORDS ? __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(i / WPR) * N) + i % WPR)
+                                 : 0u;
+            } else {   // nibble tiles 2 ct and 2 ct + 1 -> the byte's high and low nibble
+                uint32_t hi = 0u, lo = 0u;
+                if (i < WORDS) {
+                    hi = __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(2 * (i / WPR)) * N) + i % WPR);
+                    lo = __ldg(reinterpret_cast<const uint32_t *>(src + (size_t)(2 * (i / WPR) + 1) * N) + i % WPR);
+                }
+                w[j] = hi | ((lo >> 4) & 0x0F0F0F0Fu);
+            }
         }
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -516,6 +537,7 @@ __device__ __forceinline__ void bits_transpose_block(const uint8_t *__restrict__
             }
         }
     } else {
+        static_assert(TW == 8, "nibble staging only for N = 2048");
         for (int i = threadIdx.x; i < C * YB; i += blockDim.x)
             sm[i / YB][i % YB] = src[(size_t)(i / YB) * N + i % YB];
         __syncthreads();
@@ -781,7 +803,8 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     const size_t o_parts = off;
     off = align256(off + kFinWsBytes);
     const size_t o_bt = off;
-    off = align256(off + (size_t)(2 * ((n_sub + 1) / 2)) * P / 8);   // sign bytes of a frame's sub-frames
+    // staged sign bytes (one byte or nibble per tile row) of a frame's sub-frames
+    off = align256(off + (size_t)(2 * ((n_sub + 1) / 2)) * (size_t)n * (size_t)(n / ospr_col_width(n)));
     if (w) {
         w->buf = (float2 *)(base + o_buf);
         w->acc = (float *)(base + o_acc);
@@ -875,7 +898,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const int np = (npairs_total - c0) < chunk ? (npairs_total - c0) : chunk;
             const int last_sa = sf_begin + 2 * (c0 + np - 1);
             const int last_has_b = (last_sa + 1) < sf_end;
-            uint8_t *bt = holo_bits ? w.bt + 2 * (size_t)c0 * (P / 8) : nullptr;
+            uint8_t *bt = holo_bits ? w.bt + 2 * (size_t)c0 * BitsT<N>::BYTES_PER_SUBFRAME : nullptr;
             {
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
                 HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, prng, sf_first, np, last_has_b, w.buf, s)));

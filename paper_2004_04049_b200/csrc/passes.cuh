@@ -265,8 +265,10 @@ holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typen
         return e ? atoi(e) : 0;
     }();
     const int stages = env_stages ? env_stages : Body::kStages;
-    if (stages == 3 && N <= 1024)
-        return launch_cols_s<N, Body, 3>(id, buf, nframes, a, s);
+    if constexpr (ColPipe<N, 3, Body::kWidth>::SMEM <= 227 * 1024) {   // three stages fit
+        if (stages == 3)
+            return launch_cols_s<N, Body, 3>(id, buf, nframes, a, s);
+    }
     return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s);
 }
 

@@ -267,6 +267,24 @@ def test_ospr_c5_sampled():
         check_intensity(I[f], oracle.replay_from_bits(bits[f], n))
 
 
+def test_ospr_2048_prime_lut_all_subframes():
+    """N = 2048 (nibble-staged column tiles) with a prime LUT length, so every
+    sub-frame draws different phases (no L | N^2 degeneracy) and an unpaired tail: all bits
+    against the oracle (P-3), the intensity conditionally (P-4) and the MSE (P-5)."""
+    n, S, L, off = 2048, 3, 10007, 987654321
+    T = blobs_target(11, n, 16, n / 16, n / 6.4, Region.upper_half(n))
+    lg, lo = lut_pair(LUT_SEED, L)
+    om = Region.upper_half(n).as_tuple()
+    res = hb.ospr_generate(cuda_target(T), S, lg, phase_offset=off, omega=om)
+    bits, I = to_np(res.bits)[0], to_np(res.intensity)[0]
+    for s in range(S):
+        _, h_re, _ = oracle.ospr_subframe(T, lo, off + s * n * n, want_h=True, want_intensity=False)
+        check_bits(bits[s], h_re, n)
+    check_intensity(I, oracle.replay_from_bits(bits, n))
+    _, _, mse_ref = oracle.ospr(T[None], S, lo, off, om)
+    assert rel(to_np(res.mse)[0], mse_ref[0]) <= REL_TOL
+
+
 def test_ospr_chunked_equals_single_chunk(monkeypatch):
     """Several chunks of pairs (a ragged last one, the odd unpaired tail, accumulation
     across chunks) give the same holograms as one chunk, and the same intensity up to
