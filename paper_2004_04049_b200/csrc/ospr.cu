@@ -386,7 +386,7 @@ __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
 }
 
 // Columns per OSPR column-pass tile (see OsprColBody::kWidth); host and device agree on it.
-constexpr int ospr_col_width(int n) { return n >= 2048 ? 4 : 8; }
+constexpr int ospr_col_width(int n) { return n >= 1024 ? 4 : 8; }
 
 template <int N>
 struct OsprColBody {
