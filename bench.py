@@ -52,6 +52,7 @@ def parse():
                     help="N > 1: each rank its own C3 frame set (weak, no collective; default) or one frame "
                          "set's sub-frames split across ranks + NCCL all-reduce of the intensity (strong)")
     ap.add_argument("--no-gs", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gs-steps", type=int, default=None)
@@ -541,6 +542,38 @@ def run_gpu(args):
                          "what": "pinned host target -> device, a0 LUT build, ospr_generate (a1-a7), packed "
                                  "holograms + MSE -> host; " + ("CUDA graphs (memcpy + kernel nodes)"
                                                                 if use_graph else "eager")}
+
+    # ---------------- OSPR C5 frame sets (2048^2, N_SF = 32) ----------------
+    if not args.no_c5 and frames_mode:
+        w5 = WORKLOADS["C5"]
+        n5, S5, P5 = w5.n, w5.n_sub, w5.n * w5.n
+        T5 = torch.from_numpy(target_for(w5, rank)).to(dev)     # rank r: frame r of the video
+        lut5 = torch.empty(w5.lut_lens[0], dtype=torch.complex64, device=dev)
+        ws5 = torch.empty(hb.ospr_workspace_bytes(n5, 1, S5), dtype=torch.uint8, device=dev)
+        out5 = hb.OsprResult(bits=torch.empty((1, S5, n5, n5 // 8), dtype=torch.uint8, device=dev),
+                             intensity=torch.empty((1, n5, n5), dtype=torch.float32, device=dev),
+                             mse=torch.empty(1, dtype=torch.float64, device=dev))
+
+        def c5_step():
+            hb.lut_generate(LUT_SEED, w5.lut_lens[0], out=lut5)
+            hb.ospr_generate(T5, S5, lut5, phase_offset=rank * S5 * P5, workspace=ws5, out=out5)
+        k5 = max(3, args.steps // 4)
+        tm5, _ = timed_loop(graphed(c5_step, use_graph), k5, min(args.warmup, 3), world, flush)
+        tm5 = max_over_ranks(tm5, world)
+        np5 = (S5 + 1) // 2
+        bytes5 = 32 * P5 * np5 + 4 * P5 + 12 * P5 + 3 * S5 * P5 / 8   # passes A-C + finalize + sign bytes
+        result["c5"] = {
+            "metric": "OSPR 2048^2 binary sub-frames/s", "unit": UNIT,
+            "value": world * S5 * k5 / (tm5 / 1e3), "ms_per_step": tm5 / k5, "steps": k5,
+            "scaling": "weak", "mse": float(out5.mse.item()),
+            "step_hbm": {"algorithmic_bytes": bytes5, "achieved_gbs": bytes5 / (tm5 / k5 * 1e-3) / 1e9,
+                         "frac": bytes5 / (tm5 / k5 * 1e-3) / 1e9 / hbm_peak},
+            "config": {"workload": "C5 frame set: OSPR 2048x2048 binary, N_SF=32, LUT 2^16, one video frame per "
+                                   "step and GPU (a0 + a1-a7); BASELINE configs[4] (its 60-frame video is 60 such "
+                                   "steps)", "l2": "flushed before every timed step",
+                       "launch": "CUDA graph replay" if use_graph else "eager launches"},
+        }
+        del ws5
 
     # ---------------- GS C4 ----------------
     if not args.no_gs:
