@@ -16,6 +16,7 @@ CLASSES = [("ospr_rows_a_kernel", "ospr_rows_a"), ("ospr_rows_a2_kernel", "ospr_
            ("gs_rows_kernel", "gs_rows")]
 
 rep, src = sys.argv[1], sys.argv[2]
+merge = "--merge" in sys.argv[3:]   # keep the classes this report does not contain
 out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, units, vals = rows[0], rows[1], rows[2:]
@@ -37,5 +38,11 @@ for v in vals:
 for e in res.values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / e["launches"]
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+if merge and os.path.exists(path):
+    old = json.load(open(path))
+    kern = old.get("kernels", {})
+    kern.update(res)
+    res = kern
+    src = old.get("source", "") + "; " + src
 json.dump({"source": src, "kernels": res}, open(path, "w"), indent=1)
 print(json.dumps(res, indent=1))
