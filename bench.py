@@ -648,6 +648,27 @@ def _oracle_frame_set(T, lut, S, region, threads):
     return oracle.mse_m1(I, T, region)
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_one_thread_rate(T, lut, k=2):
+    """The oracle's single-thread rate (report 1-thread and all-core rates): k
+    sub-frames of the frame set, one after another on one core."""
+    import oracle
+    n = T.shape[0]
+    t0 = time.perf_counter()
+    for s in range(k):
+        oracle.ospr_subframe(T, lut, s * n * n, want_h=False, want_intensity=True)
+    return k / (time.perf_counter() - t0)
+
+
 def cpu_baseline(L, steps=1):
     import oracle
     from holo_synth import LUT_SEED, WORKLOADS, target_for
@@ -663,7 +684,7 @@ def cpu_baseline(L, steps=1):
             "sample": f"{steps} full C3 frame set(s): {w3.n_sub} sub-frames of 1024^2 (apply_phase, radix-2 "
                       f"fp64 IDFT, sign, DFT, |.|^2) + mean + MSE, L={L}, one thread per sub-frame; "
                       f"host nproc={os.cpu_count()}",
-            "seconds": dt}
+            "seconds": dt, "cpu_model": cpu_model(), "value_1_thread": oracle_one_thread_rate(T, lut)}
 
 
 def run_reference(args):
@@ -688,13 +709,14 @@ def run_reference(args):
     v = w3.n_sub * steps / dt
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong",
+        "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C3: OSPR 1024x1024 binary, N_SF=24, one frame set per step; BASELINE configs[2]",
                    "lut_len": args.lut},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": f"{steps} C3 frame set(s) of 24 sub-frames (steps capped at 3 to bound CPU "
-                                   f"time), one thread per sub-frame, host nproc={os.cpu_count()}"},
+                                   f"time), one thread per sub-frame, host nproc={os.cpu_count()}",
+                         "cpu_model": cpu_model(), "value_1_thread": oracle_one_thread_rate(T, lut)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
