@@ -100,6 +100,19 @@ def test_gs_arg_errors(L):
         _lib.HOLO_ERR_INVALID_ARG   # r_in aliases r_out
 
 
+def test_debug_pairs_arg_errors(L):
+    def call(n=64, S=4, lut=FAKE, nl=97, prng=0, b=0, e=4, z=FAKE):
+        return L.holo_debug_ospr_pairs(FAKE, n, S, lut, nl, prng, 7, 0, b, e, z, None)
+
+    assert call(n=96) == _lib.HOLO_ERR_INVALID_ARG
+    assert call(z=None) == _lib.HOLO_ERR_INVALID_ARG
+    assert call(e=5) == _lib.HOLO_ERR_INVALID_ARG              # sub-frame range outside [0, n_sub)
+    assert call(b=2, e=2) == _lib.HOLO_ERR_INVALID_ARG
+    assert call(lut=None) == _lib.HOLO_ERR_INVALID_ARG         # lut NULL but n_lut > 0
+    assert call(prng=1) == _lib.HOLO_ERR_INVALID_ARG           # the on-the-fly source excludes a LUT
+    assert b"prng" in L.holo_last_error()
+
+
 def test_workspace_sizes_monotone(L):
     assert L.holo_ospr_workspace_size(1024, 1, 24) >= 8 * 1024 * 1024 + 4 * 1024 * 1024
     assert L.holo_ospr_workspace_size(100, 1, 24) == 0
