@@ -216,8 +216,29 @@ struct LutIndexer {
             return mod_t<LUT_POW2>(a);
         return mod_t<LUT_GENERAL>(a);
     }
-    // general a (may exceed 2L): used once per row
-    __device__ __forceinline__ uint32_t mod_any(uint64_t a) const { return (uint32_t)(a % L); }
+    // a mod L for any 32-bit a (per-row bases): mask, or Lemire's fastmod with M = ceil(2^64 / L)
+    __device__ __forceinline__ uint32_t mod32(uint32_t a) const
+    {
+        if ((L & (L - 1)) == 0)
+            return a & (L - 1);
+        return (uint32_t)__umul64hi(M * (uint64_t)a, (uint64_t)L);
+    }
+    // a mod L for any 64-bit a (per-sub-frame bases): Barrett with B = floor(2^64 / L) = M - 1
+    // (L not a power of two); q = floor(a B / 2^64) is floor(a / L) or one less, so a single
+    // conditional subtract finishes.  A hardware-free replacement of the 64-bit '%' subroutine,
+    // whose dependent chain cost thousands of cycles per warp unit in pass A.
+    __device__ __forceinline__ uint32_t mod64(uint64_t a) const
+    {
+        if ((L & (L - 1)) == 0)
+            return (uint32_t)(a & (uint64_t)(L - 1));
+        const uint64_t q = __umul64hi(a, M - 1);
+        uint64_t r = a - q * (uint64_t)L;
+        if (r >= L)
+            r -= L;
+        return (uint32_t)r;
+    }
+    // general a (may exceed 2L)
+    __device__ __forceinline__ uint32_t mod_any(uint64_t a) const { return mod64(a); }
 };
 
 // Phase factor for pool entry idx.

@@ -76,7 +76,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
     float2 *S = state + (size_t)fr * P;
     uint32_t base = 0;
     if (lut != nullptr)
-        base = (uint32_t)(((uint64_t)off_mod + ((frame0 + fr) % ix.L) * (uint64_t)p_mod) % ix.L);
+        base = ix.mod64((uint64_t)off_mod + (uint64_t)ix.mod64(frame0 + fr) * (uint64_t)p_mod);
     double s[2] = {0.0, 0.0};
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
         const float t = __ldg(Tf + p);

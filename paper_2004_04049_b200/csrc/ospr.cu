@@ -55,9 +55,9 @@ constexpr size_t kFinWsBytes = (size_t)kFinBlocks * 5 * sizeof(double) + 256;   
 // so that F^-1{Z} = 2 (Re H_a + i Re H_b) after pass A.
 // Draw base of global sub-frame s: (off + s * N^2) mod L with off, N^2 reduced mod L on the
 // host (all operands < 2^31, so the 64-bit product cannot overflow).
-__device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, uint32_t p_mod, uint32_t L)
+__device__ __forceinline__ uint32_t subframe_base(uint32_t off_mod, uint64_t s, uint32_t p_mod, const LutIndexer &ix)
 {
-    return (uint32_t)(((uint64_t)off_mod + (s % L) * (uint64_t)p_mod) % L);
+    return ix.mod64((uint64_t)off_mod + (uint64_t)ix.mod64(s) * (uint64_t)p_mod);
 }
 
 // conj(Z) at the pixel pair {p1, p2 = -p1} of one sub-frame pair (a, b) from T (t1, t2) and the
@@ -78,9 +78,9 @@ __device__ __forceinline__ ZPair z_pair(float t1, float t2, float tb1, float tb2
 }
 
 // LUT index base of row y of a sub-frame whose draws start at base: (base + y N) mod L.
-__device__ __forceinline__ uint32_t row_base(uint32_t base, int y, int n, uint32_t L)
+__device__ __forceinline__ uint32_t row_base(uint32_t base, int y, int n, const LutIndexer &ix)
 {
-    return (uint32_t)(((uint64_t)base + (uint64_t)y * (uint64_t)n) % L);
+    return ix.mod32(base + (uint32_t)y * (uint32_t)n);   // base < L < 2^31, y n < 2^22: no overflow
 }
 
 // ---- pass A: randomisation (a1, a2) with Hermitian pairing, fused into the row IFFT --------------
@@ -121,14 +121,14 @@ struct PhaseRows {
         if constexpr (LMODE == LUT_PRNG)
             return ps.off + s * (uint64_t)N * N;
         else
-            return subframe_base(ps.off_mod, s, ps.p_mod, ps.ix.L);
+            return subframe_base(ps.off_mod, s, ps.p_mod, ps.ix);
     }
     static __device__ __forceinline__ Base row(const PhaseSrc &ps, Base sb, int y)
     {
         if constexpr (LMODE == LUT_PRNG)
             return sb + (uint64_t)y * N;
         else
-            return row_base(sb, y, N, ps.ix.L);
+            return row_base(sb, y, N, ps.ix);
     }
     static __device__ __forceinline__ float2 at(const PhaseSrc &ps, Base rb, int x)
     {
