@@ -770,7 +770,9 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static int ospr_chunk_pairs(int n, int n_sub)
 {
     const size_t frame = (size_t)n * n * sizeof(float2);
-    size_t budget = 96ull << 20;   // pair buffers kept L2-resident between passes (C3: one chunk)
+    // pair-buffer budget: fewer, larger chunks win (each chunk costs three launches with their
+    // ramps; L2 residency of smaller chunks measured no gain): C3 and C5 run as one chunk
+    size_t budget = 1ull << 30;
     if (const char *e = getenv("HOLO_OSPR_CHUNK_BYTES"))
         budget = strtoull(e, nullptr, 10);
     long c = (long)(budget / frame);

@@ -146,7 +146,9 @@ def test_product_package_does_not_import_oracle():
 
 
 def test_plan_queries(L):
-    assert L.holo_ospr_chunk_pairs(1024, 24) == 12          # C3: one L2-sized chunk of 12 pairs
+    assert L.holo_ospr_chunk_pairs(1024, 24) == 12          # C3: one chunk of 12 pairs
+    assert L.holo_ospr_chunk_pairs(2048, 32) == 16          # C5: one chunk of 16 pairs (512 MiB)
+    assert L.holo_ospr_chunk_pairs(2048, 200) == 32         # capped by the 1 GiB budget
     assert L.holo_ospr_chunk_pairs(64, 7) == 4
     assert L.holo_ospr_chunk_pairs(100, 7) == 0 and L.holo_ospr_chunk_pairs(64, 0) == 0
     assert L.holo_gs_group_frames(1024, 64) == 64
