@@ -240,12 +240,25 @@ struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
 
+// Barrier of a transform whose threads span warps (WS = false): the whole CTA (id = 0) or a
+// named barrier over the n threads of one consumer group (id > 0; grouped column pipeline).
+struct GroupSync {
+    int id = 0, n = 0;
+    __device__ __forceinline__ void operator()() const
+    {
+        if (id == 0)
+            __syncthreads();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    }
+};
+
 // `after_exchange` runs once every value has been read back from the exchange buffer, before
 // the pass-2 DFT: a caller refilling the buffer by TMA from there on must first order those
 // reads before the async-proxy write (fence.proxy.async + __syncwarp; WS = true only).
 template <int N, bool INV, int IL, bool WS, class TwSrc, class Hook = NoHook>
 __device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *sm, int t, const TwSrc &tws,
-                                              const Hook &after_exchange = Hook())
+                                              const Hook &after_exchange = Hook(), const GroupSync &gs = GroupSync())
 {
     using P = Plan<N>;
     constexpr int R1 = P::R1, R2 = P::R2, Q = P::Q;
@@ -255,7 +268,7 @@ __device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *s
     if (WS)
         __syncwarp();
     else
-        __syncthreads();                    // previous readers of sm are done
+        gs();                               // previous readers of sm are done
 #pragma unroll
     for (int b = 0; b < Q; ++b)
 #pragma unroll
@@ -266,7 +279,7 @@ __device__ __forceinline__ void fft2pass_impl(float2 (&v)[Plan<N>::E], float2 *s
     if (WS)
         __syncwarp();
     else
-        __syncthreads();
+        gs();
 #pragma unroll
     for (int r = 0; r < R2; ++r) {
         const int i = t + R1 * r;
@@ -324,11 +337,12 @@ struct ColFft2 {
     using P = Plan<N>;
     static constexpr int E = P::E, T = P::T, SMEM = P::SMEM;
     Twiddles<N, REG> tw;
+    GroupSync sync;                          // CTA-wide unless the pipeline runs consumer groups
     __device__ __forceinline__ void init(const float2 *twp, int t) { tw.load(twp, t); }
     template <bool INV, int IL>
     __device__ __forceinline__ void run(float2 (&v)[E], float2 *sm, int t) const
     {
-        fft2pass<N, INV, IL, false>(v, sm, t, tw);
+        fft2pass_impl<N, INV, IL, false>(v, sm, t, TwRegs<N, REG>{tw}, NoHook(), sync);
     }
 };
 

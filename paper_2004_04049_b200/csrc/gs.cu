@@ -105,6 +105,7 @@ template <int N, bool QUANT>
 struct GsColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     static constexpr int kWidth = 8;   // columns per tile (4 measured 6 % slower for this body)
+    static constexpr int kGroups = 1;
     struct Args {
         const float2 *tw;
         float2 *buf;          // the group's state (updated in place)

@@ -9,6 +9,7 @@ template <int N, bool INV>
 struct HookColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     static constexpr int kWidth = 8;   // columns per tile
+    static constexpr int kGroups = 1;
     struct Args {
         const float2 *tw;
         float2 *buf;

@@ -395,6 +395,7 @@ struct OsprColBody {
     // so that three 2048-row stages fit in shared memory and the ring overlaps load, transform
     // and store (an 8-column tile leaves room for one stage only)
     static constexpr int kWidth = ospr_col_width(N);
+    static constexpr int kGroups = N >= 2048 ? 2 : 1;   // two consumer groups per CTA (ColPipeG2)
     struct Args {
         const float2 *tw;
         float2 *buf;
@@ -450,7 +451,7 @@ struct OsprColBody {
         if (a.bits != nullptr) {
             constexpr int RG = E < 8 ? 1 : E / 8, RPG = E < 8 ? E : 8, TASKS = 2 * R1 * RG;
 #pragma unroll 1
-            for (int task = threadIdx.x; task < TASKS; task += W * R1) {
+            for (int task = t * W + c; task < TASKS; task += W * R1) {   // t W + c: thread within the group
                 const int f = task / (R1 * RG), rem = task % (R1 * RG), tt = rem % R1, rb = rem / R1;
                 if (f == 1 && !has_b)
                     continue;

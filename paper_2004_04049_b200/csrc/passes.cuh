@@ -241,6 +241,95 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
         tma::bulk_wait<0>();               // stores complete before the CTA retires
 }
 
+// Grouped variant (N = 2048, where one W-column tile's transform needs E = 64 values per thread
+// and a single 4-warp CTA per SM is all the register file and shared memory allow otherwise):
+// two consumer groups of W*T threads share one three-buffer ring.  Group g takes the CTA's
+// tiles k = g, g + 2, ... (buffer k % 3), syncs on its own named barrier, and its leader stores
+// tile k, waits for the store to read out, and refills the same buffer with tile k + 3, which
+// the other group transforms next-but-one.  Twice the warps of the plain pipeline per SM.
+template <int N, class Body>
+struct ColPipeG2 {
+    using CP = ColPipe<N, 3, Body::kWidth>;
+    static constexpr int GROUPS = 2, S = 3;
+    static constexpr int GT = CP::THREADS, THREADS = GROUPS * GT;
+    static constexpr size_t BAR_OFFSET = CP::BAR_OFFSET;
+    static constexpr size_t SCRATCH_OFFSET = BAR_OFFSET + 64;
+    static constexpr size_t SMEM = SCRATCH_OFFSET + GROUPS * CP::SCRATCH_BYTES;
+};
+
+template <int N, class Body>
+__global__ void __launch_bounds__(ColPipeG2<N, Body>::THREADS, 1)
+col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
+{
+    HOLO_PDL_ENTRY();
+    using G = ColPipeG2<N, Body>;
+    using CP = typename G::CP;
+    using F = typename CP::F;
+    constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME, S = G::S, GT = G::GT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + G::BAR_OFFSET);
+    const int g = threadIdx.x / GT, lt = threadIdx.x % GT;
+    uint32_t *scratch = reinterpret_cast<uint32_t *>(smem_raw + G::SCRATCH_OFFSET + (size_t)g * CP::SCRATCH_BYTES);
+    const int c = lt % W, t = lt / W;
+    F fft;
+    fft.init(a.tw, t);
+    fft.sync.id = 1 + g;
+    fft.sync.n = GT;
+    const fft::GroupSync gsync = fft.sync;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s)
+            tma::mbar_init(&bars[s], 1);
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int tile, int s) {
+        const int fr = tile / TPF, ct = tile % TPF;
+        tma::mbar_arrive_expect_tx(&bars[s], CP::TILE_BYTES);
+#pragma unroll
+        for (int q = 0; q < CP::NBOX; ++q)
+            tma::load_2d(stage0 + (size_t)s * CP::STAGE_ELEMS + q * CP::BOX_ROWS * W, &tmap, ct * W,
+                         fr * N + q * CP::BOX_ROWS, &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int j = 0; j < S; ++j) {
+            const int tile = blockIdx.x + j * gridDim.x;
+            if (tile < ntiles)
+                issue(tile, j);
+        }
+    #pragma unroll 1   // one copy of the transform code (instruction cache)
+    for (int k = g, tile = blockIdx.x + g * gridDim.x; tile < ntiles; k += 2, tile += 2 * gridDim.x) {
+        const int s = k % S;
+        float2 *st = stage0 + (size_t)s * CP::STAGE_ELEMS;
+        tma::mbar_wait(&bars[s], (uint32_t)((k / S) & 1));
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = st[(t + T * m) * W + c];
+        Body::template run<F, W>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
+        gsync();                           // every thread of the group is done with the exchange data
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            st[(t + T * m) * W + c] = v[m];
+        tma::fence_proxy_async_smem();     // generic writes before the async-proxy store
+        gsync();
+        if (lt == 0) {
+            const int fr = tile / TPF, ct = tile % TPF;
+#pragma unroll
+            for (int q = 0; q < CP::NBOX; ++q)
+                tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
+            tma::bulk_commit();
+            const int nxt = tile + S * gridDim.x;   // tile k + 3: this buffer's next use
+            if (nxt < ntiles) {
+                tma::bulk_wait_read<0>();           // the store has read the buffer out
+                issue(nxt, s);
+            }
+        }
+    }
+    if (lt == 0)
+        tma::bulk_wait<0>();               // stores complete before the CTA retires
+}
+
 // Host: launch the column pipeline over `nframes` frames of `buf` (row-major
 // [nframes*N][N] complex64).
 template <int N, class Body, int NSTAGES>
@@ -256,10 +345,28 @@ holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typ
     return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
 }
 
-// Body::kStages (3 or 1) picks the variant (measured per body); HOLO_COL_STAGES overrides it.
+template <int N, class Body>
+holo_status launch_cols_g2(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+{
+    using G = ColPipeG2<N, Body>;
+    using CP = typename G::CP;
+    CUtensorMap map;
+    HOLO_TRY(make_tmap_c64(&map, buf, N, (uint64_t)nframes * N, CP::W, CP::BOX_ROWS));
+    const int ntiles = nframes * CP::TILES_PER_FRAME;
+    const int grid = pipe_grid(col_pipe_g2_kernel<N, Body>, G::THREADS, G::SMEM, (ntiles + 1) / 2, 1);
+    return launch(id, col_pipe_g2_kernel<N, Body>, dim3(grid), dim3(G::THREADS), G::SMEM, s, map, ntiles, a);
+}
+
+// Body::kStages (3 or 1) picks the variant (measured per body); HOLO_COL_STAGES overrides it;
+// Body::kGroups = 2 selects the grouped pipeline.
 template <int N, class Body>
 holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
 {
+    if constexpr (Body::kGroups == 2) {
+        static const bool off = getenv("HOLO_COL_G1") != nullptr;   // experiments: the plain pipeline
+        if (!off)
+            return launch_cols_g2<N, Body>(id, buf, nframes, a, s);
+    }
     static const int env_stages = [] {
         const char *e = getenv("HOLO_COL_STAGES");
         return e ? atoi(e) : 0;
