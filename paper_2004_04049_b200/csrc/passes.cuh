@@ -250,6 +250,8 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
 template <int N, class Body>
 struct ColPipeG2 {
     using CP = ColPipe<N, 3, Body::kWidth>;
+    using F = fft::ColFft2<N, false>;         // pool twiddles: the register budget of two groups
+    static_assert(F::E == CP::E && F::T == CP::T, "same transform shape as the plain pipeline");
     static constexpr int GROUPS = 2, S = 3;
     static constexpr int GT = CP::THREADS, THREADS = GROUPS * GT;
     static constexpr size_t BAR_OFFSET = CP::BAR_OFFSET;
@@ -264,7 +266,7 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
     HOLO_PDL_ENTRY();
     using G = ColPipeG2<N, Body>;
     using CP = typename G::CP;
-    using F = typename CP::F;
+    using F = typename G::F;
     constexpr int T = CP::T, E = CP::E, W = CP::W, TPF = CP::TILES_PER_FRAME, S = G::S, GT = G::GT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stage0 = reinterpret_cast<float2 *>(smem_raw);
