@@ -22,7 +22,9 @@ from typing import Callable, Optional, Sequence, Tuple
 
 import torch
 
-from .api import OsprResult, default_omega, ospr_generate, ospr_workspace_bytes
+from . import api
+from ._lib import check, lib
+from .api import OsprResult, default_omega, ospr_workspace_bytes
 
 
 class OsprStream:
@@ -64,6 +66,16 @@ class OsprStream:
         self.h2d_done, self.comp_done, self.d2h_done = ev(), ev(), ev()
         self.used = [False] * depth
         self.f = 0
+        # per-submit host work kept small (the host must stay ahead of ~0.1 ms frame sets): views
+        # and the holo_ospr_generate arguments are prepared once per slot; only the cursor varies
+        self.t_view = [t[0] for t in self.t_dev]
+        self.bits_view = [o.bits[0] for o in self.out]
+        self.inten_view = [o.intensity[0] for o in self.out]
+        lp, L = api._lut_args(lut)
+        self._gen = lib().holo_ospr_generate
+        self._args = [(t.data_ptr(), n, 1, n_sub, lp, L) for t in self.t_dev]
+        self._tail = [(0, n_sub, o.bits.data_ptr(), o.intensity.data_ptr(), o.mse.data_ptr(), api._region(self.omega),
+                       self.ws.data_ptr(), self.ws.numel(), self.comp.cuda_stream) for o in self.out]
 
     def frame_offset(self, f: int) -> int:
         """Phase cursor of this stream's frame set f: off0 + f * frame_stride * N_SF N^2 when
@@ -82,22 +94,20 @@ class OsprStream:
             self.h2d.wait_event(self.comp_done[s])
             self.comp.wait_event(self.d2h_done[s])
         with torch.cuda.stream(self.h2d):
-            self.t_dev[s][0].copy_(target_host, non_blocking=True)
+            self.t_view[s].copy_(target_host, non_blocking=True)
             self.h2d_done[s].record(self.h2d)
         self.comp.wait_event(self.h2d_done[s])
-        with torch.cuda.stream(self.comp):
-            if self.before_each is not None:
+        if self.before_each is not None:
+            with torch.cuda.stream(self.comp):
                 self.before_each()
-            ospr_generate(self.t_dev[s], self.n_sub, self.lut, phase_offset=self.frame_offset(f),
-                          omega=self.omega, workspace=self.ws, out=self.out[s])
-            self.comp_done[s].record(self.comp)
+        check(self._gen(*self._args[s], self.frame_offset(f), *self._tail[s]))   # ospr_generate on comp
+        self.comp_done[s].record(self.comp)
         self.d2h.wait_event(self.comp_done[s])
         with torch.cuda.stream(self.d2h):
-            o = self.out[s]
-            self.bits_host[s].copy_(o.bits[0], non_blocking=True)
-            self.mse_host[s].copy_(o.mse, non_blocking=True)
+            self.bits_host[s].copy_(self.bits_view[s], non_blocking=True)
+            self.mse_host[s].copy_(self.out[s].mse, non_blocking=True)
             if self.inten_host is not None:
-                self.inten_host[s].copy_(o.intensity[0], non_blocking=True)
+                self.inten_host[s].copy_(self.inten_view[s], non_blocking=True)
             self.d2h_done[s].record(self.d2h)
         self.used[s] = True
         self.f = f + 1
