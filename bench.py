@@ -391,10 +391,13 @@ def run_gpu(args):
     nchunks = -(-npairs // chunk)
     np_l = npairs / nchunks                                      # pairs per launch (average)
     nsub_l = (se - sb) / nchunks                                 # sub-frames per launch
+    fused_a7 = "ospr_finalize" not in kern                       # N >= 1024: a7 runs inside pass C
     alg_bytes = {                                                # DESIGN.md §7 table
         "ospr_rows_a": 4 * P + 8 * min(args.lut, 2 * np_l * P) + 8 * P * np_l,
         "ospr_cols": 16 * P * np_l + nsub_l * P / 8,
-        "ospr_rows_c": 8 * P * np_l + 4 * P + (4 * P if nchunks > 1 else 0) * (nchunks - 1) / nchunks,
+        # pass C: pair rows in; fused a7: T in, intensity out, sign bytes -> packed holograms
+        "ospr_rows_c": (8 * P * np_l + 8 * P + 2 * (se - sb) * P / 8) if fused_a7 else
+                       (8 * P * np_l + 4 * P + (4 * P if nchunks > 1 else 0) * (nchunks - 1) / nchunks),
         "ospr_finalize": 12 * P + 2 * (se - sb) * P / 8,             # + sign bytes -> packed holograms
     }
     dom = max((k for k in kern if k in alg_bytes), key=lambda k: kern[k]["total_ms"])

@@ -142,9 +142,11 @@ struct PhaseRows {
 template <int N, int LMODE, bool ZOUT = false>
 __global__ void __launch_bounds__(RowA<N>::WPC * 32)
 ospr_rows_a_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
-                   int npairs, int last_pair_has_b, float2 *__restrict__ buf)
+                   int npairs, int last_pair_has_b, float2 *__restrict__ buf, unsigned *zc)
 {
     HOLO_PDL_ENTRY();
+    if (zc != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+        *zc = 0u;                        // the frame's fused-finalize ticket (pass C, last chunk)
     using P = fft::Plan<N>;
     using RA = RowA<N>;
     using PR = PhaseRows<N, LMODE>;
@@ -275,9 +277,11 @@ struct RowA2 {
 template <int N, int LMODE, bool ZOUT = false>
 __global__ void __launch_bounds__(RowA2<N>::WPC * 32)
 ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
-                    int npairs, int last_pair_has_b, float2 *__restrict__ buf)
+                    int npairs, int last_pair_has_b, float2 *__restrict__ buf, unsigned *zc)
 {
     HOLO_PDL_ENTRY();
+    if (zc != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+        *zc = 0u;                        // the frame's fused-finalize ticket (pass C, last chunk)
     using P = fft::Plan<N>;
     using RA = RowA2<N>;
     using PR = PhaseRows<N, LMODE>;
@@ -698,6 +702,160 @@ __device__ __forceinline__ double mse_from_sums(const double *o, double inv_coun
     return (sum > 0.0 ? sum : 0.0) * inv_count;
 }
 
+// ---- pass C + a7 for the frame's last chunk (N >= 1024): mirrored row pairs per CTA ----------
+// Unit u covers rows {u, N - u} (u = 0: rows 0 and N/2, each its own mirror).  Warps 0-1 take
+// row ya = u, warps 2-3 row yb (pairs split between the two warps of a row, as in pass C).  With
+// both rows' |X|^2 sums in shared memory the CTA symmetrises (I[k] = (A[k] + A[-k]) s), writes
+// the two intensity rows and its five fp64 MSE partials, and the last CTA (ticket) reduces the
+// N/2 partials in unit order.  No accumulator round trip through HBM and no finalize launch;
+// the T rows are fetched at CTA start, so the epilogue waits on shared memory only.
+template <int N>
+struct RowCF {
+    using P = fft::Plan<N>;
+    static_assert(32 / P::T == 1, "one row per warp");
+    static constexpr int NU = N / 2, THREADS = 128;
+    static constexpr uint32_t IN_BYTES = (uint32_t)N * 8, SLOT = RowC<N>::SLOT;
+    static constexpr size_t SA = 4 * (size_t)SLOT;                 // A rows ya, yb (fp32)
+    static constexpr size_t SMEM = SA + 2 * (size_t)N * sizeof(float) + 4 * sizeof(uint64_t);
+};
+
+template <int N>
+__global__ void __launch_bounds__(RowCF<N>::THREADS, N <= 1024 ? 4 : 1)   // N = 1024: 512 units in one wave
+ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
+                    const float *__restrict__ acc_in, const float *__restrict__ T, float scale, float *__restrict__ out,
+                    holo_region om, double *__restrict__ parts, unsigned *ticket, double inv_count,
+                    double *__restrict__ mse, int nbt, const uint8_t *__restrict__ bt, uint8_t *__restrict__ bits)
+{
+    HOLO_PDL_ENTRY();
+    if ((int)blockIdx.x < nbt) {         // the frame's sign-byte transposes, scheduled first
+        const int j = (int)blockIdx.x;
+        bits_transpose_block<N, RowCF<N>::THREADS>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
+        return;
+    }
+    using P = fft::Plan<N>;
+    using RC = RowCF<N>;
+    constexpr int R1 = P::R1, E = P::E, NU = RC::NU, PER = N / RC::THREADS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = lane, half = warp & 1, side = warp >> 1;
+    const int u = (int)blockIdx.x - nbt;
+    const int ya = u, yb = u > 0 ? N - u : N / 2;
+    const int y = side ? yb : ya;
+    float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RC::SLOT);
+    float *sA = reinterpret_cast<float *>(smem_raw + RC::SA);           // [2][N]: A of ya, yb
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + RC::SA + 2 * (size_t)N * sizeof(float)) + warp;
+    // T of both rows (inputs, not produced by the previous pass), in flight during the transforms
+    float ta[PER], tb[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        ta[j] = __ldg(T + (size_t)ya * N + threadIdx.x + RC::THREADS * j);
+        tb[j] = __ldg(T + (size_t)yb * N + threadIdx.x + RC::THREADS * j);
+    }
+    const int hp = (npairs + 1) / 2, p0 = half * hp, p1 = half ? npairs : hp;
+    auto src = [&](int p) { return buf + ((size_t)p * N + (size_t)y) * N; };
+    if (lane == 0) {
+        tma::mbar_init(bar, 1);
+        tma::fence_mbar_init();
+    }
+    __syncwarp();
+    if (lane == 0 && p0 < p1) {
+        tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
+        tma::load_1d(sl, src(p0), RC::IN_BYTES, bar);
+    }
+    float a[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        a[r] = 0.0f;
+    uint32_t k = 0;
+    #pragma unroll 1
+    for (int p = p0; p < p1; ++p, ++k) {
+        tma::mbar_wait(bar, k & 1u);
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = sl[t + R1 * m];
+        const bool more = p + 1 < p1;
+        const float2 *nx = src(p + 1);
+        fft::fft2pass_hook<N, false, 1, true>(v, sl, t, tw, [&] {
+            tma::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && more) {
+                tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
+                tma::load_1d(sl, nx, RC::IN_BYTES, bar);
+            }
+        });
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            a[r] = __fmaf_rn(v[r].x, v[r].x, __fmaf_rn(v[r].y, v[r].y, a[r]));
+    }
+    // A row = (half 0 + half 1) / N^2 (+ earlier chunks' sums), fixed order as in pass C
+    float *rowA = sA + (size_t)side * N;
+    if (half == 1) {
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            rowA[t + R1 * r] = a[r];
+    }
+    __syncthreads();
+    if (half == 0) {
+        constexpr float inv_p = 1.0f / ((float)N * (float)N);   // exact power of two
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int x = t + R1 * r;
+            const float val = (a[r] + rowA[x]) * inv_p;
+            rowA[x] = acc_in != nullptr ? acc_in[(size_t)y * N + x] + val : val;
+        }
+    }
+    __syncthreads();
+    // a7: symmetrise both rows, write the mean intensity, fp64 MSE partials (R-12) over Omega
+    double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const float *A0 = sA, *A1 = sA + N;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int r = h ? yb : ya;
+        // the mirror of (r, x) is (N - r, N - x): row yb for ya (u > 0), or the row itself (u = 0)
+        const float *own = h ? A1 : A0, *mir = (u > 0) ? (h ? A0 : A1) : own;
+        const bool row_in = r >= om.row0 && r < om.row1;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int x = threadIdx.x + RC::THREADS * j;
+            const float I = (own[x] + mir[(N - x) & (N - 1)]) * scale;   // as ospr_finalize_kernel
+            out[(size_t)r * N + x] = I;
+            if (mse != nullptr && row_in && x >= om.col0 && x < om.col1) {
+                const double Id = I, tt = h ? tb[j] : ta[j], t2 = tt * tt;
+                s[0] += Id;
+                s[1] += Id * Id;
+                s[2] += Id * t2;
+                s[3] += t2;
+                s[4] += t2 * t2;
+            }
+        }
+    }
+    if (mse == nullptr)
+        return;
+    block_reduce_store(s, 5, parts + (size_t)u * 5);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();                                   // this unit's partials before its ticket
+        last = atomicAdd(ticket, 1u) == (unsigned)NU - 1u;
+    }
+    __syncthreads();
+    if (!last)
+        return;
+    __threadfence();
+    double tsum[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < NU; b += blockDim.x)
+        for (int i = 0; i < 5; ++i)
+            tsum[i] += __ldcg(parts + (size_t)b * 5 + i);
+    __shared__ double o[5];
+    __syncthreads();
+    block_reduce_store(tsum, 5, o);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *mse = mse_from_sums(o, inv_count);
+        *ticket = 0u;
+    }
+}
+
+
 // intensity[k] = (A[k] + A[-k]) * scale (symmetrise = 1) or A[k] * scale; optional fp64
 // partial sums (sum I, sum I^2, sum I T^2, sum T^2, sum T^4) over Omega, one slot per CTA.
 // With mse != NULL the last CTA to finish (atomic ticket on *counter, which the host zeroes
@@ -791,7 +949,8 @@ struct OsprWs {
     float2 *buf;
     float *acc;
     double *parts;
-    uint8_t *bt;   // tile-major sign bytes of a chunk
+    uint8_t *bt;        // tile-major sign bytes of a chunk
+    double *cf_parts;   // fused a7 (N >= 1024): [N/2][5] unit partial sums, then the ticket
 };
 
 static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
@@ -808,7 +967,10 @@ static size_t ospr_ws_layout(int n, int n_sub, char *base, OsprWs *w)
     const size_t o_bt = off;
     // staged sign bytes (one byte or nibble per tile row) of a frame's sub-frames
     off = align256(off + (size_t)(2 * ((n_sub + 1) / 2)) * (size_t)n * (size_t)(n / ospr_col_width(n)));
+    const size_t o_cf = off;
+    off = align256(off + (size_t)(n / 2) * 5 * sizeof(double) + 64);
     if (w) {
+        w->cf_parts = (double *)(base + o_cf);
         w->buf = (float2 *)(base + o_buf);
         w->acc = (float *)(base + o_acc);
         w->parts = (double *)(base + o_parts);
@@ -842,7 +1004,7 @@ holo_status finalize_frame(const float *acc, const float *T, int symmetrise, flo
 // variant that stores conj(Z) instead of its row IFFT).
 template <int N, bool ZOUT>
 static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseSrc &ps, bool prng, uint64_t sf_first,
-                                 int np, int last_has_b, float2 *buf, cudaStream_t s)
+                                 int np, int last_has_b, float2 *buf, cudaStream_t s, unsigned *zc = nullptr)
 {
     if constexpr (N >= 1024) {
         using RA2 = RowA2<N>;
@@ -852,7 +1014,7 @@ static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseS
                                            : ospr_rows_a2_kernel<N, LUT_GENERAL, ZOUT>;
         const int grid = pipe_grid(kern, RA2::WPC * 32, RA2::SMEM, np * RA2::UNITS_PER_PAIR, RA2::UPC);
         return launch(ZOUT ? K_RANDOMISE : K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA2::WPC * 32), RA2::SMEM, s, tw,
-                      Tf, ps, sf_first, np, last_has_b, buf);
+                      Tf, ps, sf_first, np, last_has_b, buf, zc);
     } else {
         using RA = RowA<N>;
         auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG, ZOUT>
@@ -861,7 +1023,7 @@ static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseS
                                            : ospr_rows_a_kernel<N, LUT_GENERAL, ZOUT>;
         const int grid = pipe_grid(kern, RA::WPC * 32, RA::SMEM, np * RA::UNITS_PER_PAIR, RA::WPC);
         return launch(ZOUT ? K_RANDOMISE : K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::WPC * 32), RA::SMEM, s, tw, Tf,
-                      ps, sf_first, np, last_has_b, buf);
+                      ps, sf_first, np, last_has_b, buf, zc);
     }
 }
 
@@ -895,6 +1057,9 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     PhaseSrc ps;
     HOLO_TRY(make_phase_src(N, lut, n_lut, prng, seed, phase_offset, &ps));
+    // a7 fused into the last chunk's pass C when one warp owns a row (N >= 1024); else its own kernel
+    constexpr bool kFuse = RowC<N>::GPW == 1;
+    const float scale = full ? 0.5f / (float)n_sub : 0.5f;
     for (int f = 0; f < n_frames; ++f) {
         const float *Tf = target + (size_t)f * P;
         for (int c0 = 0; c0 < npairs_total; c0 += chunk) {
@@ -902,15 +1067,31 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const int last_sa = sf_begin + 2 * (c0 + np - 1);
             const int last_has_b = (last_sa + 1) < sf_end;
             uint8_t *bt = holo_bits ? w.bt + 2 * (size_t)c0 * BitsT<N>::BYTES_PER_SUBFRAME : nullptr;
+            unsigned *cf_ticket = reinterpret_cast<unsigned *>(w.cf_parts + (size_t)(N / 2) * 5);
+            const bool last = c0 + np >= npairs_total;
             {
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, prng, sf_first, np, last_has_b, w.buf, s)));
+                HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, prng, sf_first, np, last_has_b, w.buf, s,
+                                                  (kFuse && last) ? cf_ticket : nullptr)));
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
             HOLO_TRY((launch_cols<N, OsprColBody<N>>(K_OSPR_COLS, w.buf, np, ca, s)));
-            {
+            bool fused = false;
+            if constexpr (kFuse) {
+                if (last) {   // pass C + a7 fused: mirrored row pairs per CTA
+                fused = true;
+                using RC = RowCF<N>;
+                const int nbt = holo_bits ? nsh * BitsT<N>::BLOCKS_PER_Q : 0;
+                const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
+                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_cf_kernel<N>, dim3(nbt + RC::NU), dim3(RC::THREADS), RC::SMEM,
+                                s, tw, (const float2 *)w.buf, np, c0 > 0 ? (const float *)w.acc : (const float *)nullptr,
+                                Tf, scale, intensity + (size_t)f * P, om, w.cf_parts, cf_ticket, 1.0 / cnt,
+                                (full && mse) ? mse + f : (double *)nullptr, nbt, (const uint8_t *)w.bt,
+                                holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr));
+                }
+            }
+            if (!fused) {
                 using RC = RowC<N>;
-                const bool last = c0 + np >= npairs_total;
                 const int nbt = (last && holo_bits) ? nsh * BitsT<N>::BLOCKS_PER_Q : 0;
                 const int grid = pipe_grid(ospr_rows_c_kernel<N>, 64, RC::SMEM, RC::NGRP, 1);
                 HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows_c_kernel<N>, dim3(nbt + grid), dim3(64), RC::SMEM, s, tw,
@@ -918,9 +1099,9 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                                 (const uint8_t *)w.bt, holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr));
             }
         }
-        const float scale = full ? 0.5f / (float)n_sub : 0.5f;
-        HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
-                                   (full && mse) ? mse + f : nullptr, s, true));
+        if (!kFuse)
+            HOLO_TRY(finalize_frame<N>(w.acc, Tf, 1, scale, intensity + (size_t)f * P, om, w.parts,
+                                       (full && mse) ? mse + f : nullptr, s, true));
     }
     return HOLO_OK;
 }
