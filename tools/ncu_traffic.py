@@ -11,7 +11,8 @@ import sys
 # ncu kernel-name prefix -> libholo kernel class (csrc/runtime.cu kKernelNames)
 CLASSES = [("ospr_rows_a_kernel", "ospr_rows_a"), ("ospr_rows_a2_kernel", "ospr_rows_a"), ("col_pipe_kernel<1024, holo::OsprColBody", "ospr_cols"),
            ("col_pipe_kernel<1024, OsprColBody", "ospr_cols"), ("ospr_bits_transpose", "ospr_bits"),
-           ("ospr_rows_c_kernel", "ospr_rows_c"), ("ospr_finalize_kernel", "ospr_finalize"),
+           ("ospr_rows_c_kernel", "ospr_rows_c"), ("ospr_rows_cf_kernel", "ospr_rows_c"),
+           ("ospr_finalize_kernel", "ospr_finalize"),
            ("col_pipe_kernel<1024, holo::GsColBody", "gs_cols"), ("col_pipe_kernel<1024, GsColBody", "gs_cols"),
            ("gs_rows_kernel", "gs_rows")]
 
