@@ -135,9 +135,9 @@ holo_status holo_lut_generate(uint64_t seed, uint64_t n_lut, holo_c64 *lut, holo
 size_t holo_ospr_workspace_size(int32_t n, int32_t n_frames, int32_t n_sub);
 
 /* Plan query (instrumentation): the number of sub-frame pairs each chunk of
- * holo_ospr_generate(n, ..., n_sub, ...) transforms per pass (DESIGN.md §5,
- * L2-resident pair buffers; HOLO_OSPR_CHUNK_BYTES overrides the 96 MiB budget);
- * 0 for invalid n or n_sub. */
+ * holo_ospr_generate(n, ..., n_sub, ...) transforms per pass (DESIGN.md §5:
+ * at most 64 pairs within a 1 GiB pair-buffer budget, which
+ * HOLO_OSPR_CHUNK_BYTES overrides); 0 for invalid n or n_sub. */
 int32_t holo_ospr_chunk_pairs(int32_t n, int32_t n_sub);
 
 holo_status holo_ospr_generate(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
