@@ -727,17 +727,17 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
                     double *__restrict__ mse, int nbt, const uint8_t *__restrict__ bt, uint8_t *__restrict__ bits)
 {
     HOLO_PDL_ENTRY();
-    if ((int)blockIdx.x < nbt) {         // the frame's sign-byte transposes, scheduled first
-        const int j = (int)blockIdx.x;
-        bits_transpose_block<N, RowCF<N>::THREADS>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
-        return;
-    }
     using P = fft::Plan<N>;
     using RC = RowCF<N>;
     constexpr int R1 = P::R1, E = P::E, NU = RC::NU, PER = N / RC::THREADS;
+    if ((int)blockIdx.x >= NU) {         // the frame's sign-byte transposes, after the row-pair units:
+        const int j = (int)blockIdx.x - NU;   // they fill the slots the units leave free
+        bits_transpose_block<N, RowCF<N>::THREADS>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
+        return;
+    }
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = lane, half = warp & 1, side = warp >> 1;
-    const int u = (int)blockIdx.x - nbt;
+    const int u = (int)blockIdx.x;
     const int ya = u, yb = u > 0 ? N - u : N / 2;
     const int y = side ? yb : ya;
     float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RC::SLOT);
