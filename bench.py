@@ -465,7 +465,9 @@ def run_gpu(args):
     if not args.no_sweep and world == 1:
         sweep = {}
         big = torch.empty(max(w3.lut_lens), dtype=torch.complex64, device=dev)
-        for L in w3.lut_lens:
+        # BASELINE's lengths all divide N_SF N^2 (every sub-frame draws the same phases, SURVEY G-8);
+        # 65537 (prime) is the non-degenerate control at the same pool size
+        for L in tuple(w3.lut_lens) + (65537,):
             st = graphed(make_ospr_step(L, big), use_graph)
             tm, _ = timed_loop(st, max(3, args.steps // 2), 2, world, flush)
             sweep[str(L)] = {"sub_frames_per_s": S * max(3, args.steps // 2) / (tm / 1e3),
