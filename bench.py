@@ -500,20 +500,21 @@ def run_gpu(args):
         torch.cuda.synchronize()
         barrier(world)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(args.steps, 60)   # frame sets streamed: amortises the pipeline's fill and drain
         a.record(stream.h2d)
         first = stream.f
-        for i in range(args.steps):
+        for i in range(ke):
             stream.submit(hosts[i % 3])
         b.record(stream.d2h)
         torch.cuda.synchronize()
         barrier(world)
         tm = max_over_ranks(a.elapsed_time(b), world)
         mse_e2e = float(stream.result(stream.f - 1)[1][0])
-        result["e2e"] = {"value": world * S * args.steps / (tm / 1e3), "unit": UNIT,
+        result["e2e"] = {"value": world * S * ke / (tm / 1e3), "unit": UNIT, "frame_sets_timed": ke,
                          "h2d_bytes_per_step": world * hosts[0].numel() * 4,
                          "d2h_bytes_per_step": world * (stream.bits_host[0].numel() + 8),
                          "bytes_per_step": "all ranks (one frame set per rank per step)",
-                         "ms_per_step": tm / args.steps, "frame_sets": [first, stream.f], "mse_last": mse_e2e,
+                         "ms_per_step": tm / ke, "frame_sets": [first, stream.f], "mse_last": mse_e2e,
                          "what": "paper_2004_04049_b200.OsprStream (public API): per frame set a pinned host target "
                                  "-> device, a0 LUT build, ospr_generate (a1-a7) with the continuing cursor, packed "
                                  "holograms + MSE -> pinned host; H2D of f+1 and D2H of f-1 overlap the kernels of "
