@@ -1,6 +1,6 @@
 // gs.cu -- Gerchberg-Saxton (Fig. 2 left; steps g0-g6 of
 // DESIGN.md §1) as two fused FFT passes per iteration over groups of frames
-// whose state stays L2-resident across iterations.
+// (C4: one group of 64 frames, a 512 MiB state streamed from HBM).
 //
 //   gs_rows_init  g0: R_0 = T * lut[(base_b + p) mod L] (or a given R_{k-1} for the
 //                 one-step hook); row IFFT -> state; fp64 sums of T^2, T^4 over Omega.

@@ -451,7 +451,7 @@ struct OsprColBody {
         // bits r of words [f][t'][0..7]; a task gathers 8 rows r = 8*rb .. 8*rb+7 of one t' as
         // an 8x8 bit matrix (byte 7-c = column c) and transposes it into the 8 row bytes.  The
         // bytes go to the tile-major staging layout bt[sub-frame][ct][y] (a warp writes 32
-        // consecutive rows = one sector); the finalize kernel makes them row-major.
+        // consecutive rows = one sector); pass C's transpose CTAs make them row-major.
         if (a.bits != nullptr) {
             constexpr int RG = E < 8 ? 1 : E / 8, RPG = E < 8 ? E : 8, TASKS = 2 * R1 * RG;
 #pragma unroll 1

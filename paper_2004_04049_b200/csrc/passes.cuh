@@ -3,12 +3,14 @@
 //
 //  * row passes: each row transform is owned by the T = R1 threads of one warp
 //    (N <= 2048, so T <= 32) and synchronises with __syncwarp() only; warps run
-//    independently, loads come straight from global/L2 into registers
-//    (coalesced: lane t reads x = t + R1*m), results go straight back.
-//  * column passes: a persistent CTA streams tiles of W = 8 columns x N rows
-//    through a double-buffered shared-memory ring filled by TMA
-//    (cp.async.bulk.tensor.2d, mbarrier completion); the column transforms read
-//    the tile from shared memory, exchange in place, and write results to global.
+//    independently; rows arrive by 1D TMA (cp.async.bulk) into per-warp slots or are
+//    built in place (OSPR pass A), results go straight back (coalesced: lane t holds
+//    x = t + R1*m).
+//  * column passes: persistent CTAs stream tiles of W (8 or 4) columns x N rows
+//    through a three-stage shared-memory ring filled by TMA (cp.async.bulk.tensor.2d,
+//    mbarrier completion); the transforms read the tile from shared memory, exchange
+//    in place, and the results leave through the stage by one TMA tile store.  At
+//    N = 2048 two consumer groups per CTA share the ring (col_pipe_g2_kernel).
 #pragma once
 
 #include "fft.cuh"
