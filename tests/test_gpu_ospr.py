@@ -193,6 +193,44 @@ def test_ospr_shards_reproduce_single_call():
     assert rel(mse.item(), full.mse.item()) <= 1e-5
 
 
+@pytest.mark.parametrize("chunk_pairs", [0, 2])
+def test_ospr_fused_a7_shards_chunks_frames(monkeypatch, chunk_pairs):
+    """The fused pass C + a7 of N >= 1024 in every mode it has: whole range with MSE, shards
+    (partial sums, no MSE, odd boundaries), several frames per call (the ticket re-armed by each
+    frame's pass A) and, with 2-pair chunks, the accumulator carried into the last chunk.  The
+    shards' finalize(sum) must match the single call (P-8), and frame f must equal a single-frame
+    call at cursor f N_SF N^2 (R-2), bit for bit."""
+    if chunk_pairs:
+        monkeypatch.setenv("HOLO_OSPR_CHUNK_BYTES", str(chunk_pairs * 1024 * 1024 * 8))
+    n, S, off = 1024, 7, 321
+    Ts = np.stack([blobs_target(80 + f, n, 16, 64.0, 160.0, Region.upper_half(n)) for f in range(2)])
+    tg = cuda_target(Ts)
+    lut = hb.lut_generate(LUT_SEED, 10007)
+    full = hb.ospr_generate(tg, S, lut, phase_offset=off)
+    for f in range(2):
+        one = hb.ospr_generate(cuda_target(Ts[f]), S, lut, phase_offset=off + f * S * n * n)
+        assert torch.equal(one.bits[0], full.bits[f]) and torch.equal(one.intensity[0], full.intensity[f])
+        assert torch.equal(one.mse[0], full.mse[f])
+    acc = torch.zeros_like(full.intensity)
+    for b, e in [(0, 3), (3, 4), (4, 7)]:
+        r = hb.ospr_generate(tg, S, lut, phase_offset=off, sf_range=(b, e))
+        assert r.mse is None
+        assert torch.equal(r.bits, full.bits[:, b:e])
+        acc += r.intensity
+    mean, mse = hb.ospr_finalize(tg, acc, S)
+    d = (mean - full.intensity).abs().max().item() / full.intensity.abs().max().item()
+    assert d <= 1e-6
+    for f in range(2):
+        assert rel(mse[f].item(), full.mse[f].item()) <= 1e-5
+    # and the whole-range result against the oracle (frame 1, two sub-frames' bits, the MSE)
+    lo = oracle.lut_build(LUT_SEED, 10007)
+    bits = to_np(full.bits)
+    for s_ in (0, 6):
+        _, h_re, _ = oracle.ospr_subframe(Ts[1], lo, off + (S + s_) * n * n, want_h=True, want_intensity=False)
+        check_bits(bits[1, s_], h_re, n)
+    check_intensity(to_np(full.intensity)[1], oracle.replay_from_bits(bits[1], n))
+
+
 def test_ospr_deterministic():
     T = cuda_target(target_for(WORKLOADS["C1"]))
     lut = hb.lut_generate(LUT_SEED, 257)
