@@ -440,9 +440,13 @@ def run_gpu(args):
     }
 
     # ---------------- N > 1: one frame set split over the ranks (C-1 over NCCL) ----------------
-    if world > 1 and frames_mode and world <= S:       # every rank holds sub-frames (same collectives)
-        ssb, sse = shard_range(S, world, rank)
-        sh = ShardedOspr(world, rank)
+    # HOLO_BENCH_FAKE_SHARDS=k (testing only, N = 1): run this block as rank 0 of k with a no-op
+    # collective, to exercise its code path on one GPU; its number is not a result
+    fake_sh = int(os.environ.get("HOLO_BENCH_FAKE_SHARDS", "0")) if world == 1 else 0
+    sh_world = fake_sh if fake_sh > 1 else world
+    if sh_world > 1 and frames_mode and sh_world <= S:   # every rank holds sub-frames (same collectives)
+        ssb, sse = shard_range(S, sh_world, rank)
+        sh = ShardedOspr(sh_world, rank, all_reduce=(lambda t: None)) if fake_sh > 1 else ShardedOspr(world, rank)
         s_out = hb.OsprResult(bits=torch.empty((1, sse - ssb, n, n // 8), dtype=torch.uint8, device=dev),
                               intensity=torch.empty((1, n, n), dtype=torch.float32, device=dev), mse=None)
         s_mse = torch.empty(1, dtype=torch.float64, device=dev)
@@ -457,7 +461,7 @@ def run_gpu(args):
         result["subframe_shards"] = {
             "value": S * args.steps / (stm / 1e3), "unit": UNIT, "ms_per_step": stm / args.steps,
             "scaling": "strong", "mse": float(s_mse.item()),
-            "what": f"one C3 frame set per step, its {S} sub-frames split over {world} ranks "
+            "what": f"one C3 frame set per step, its {S} sub-frames split over {sh_world} ranks "
                     "(shard_range), NCCL all-reduce of the partial intensity, then mean + MSE on every rank "
                     "(BASELINE configs[4]'s partition; graphs around the eager all-reduce)"}
 
