@@ -437,3 +437,41 @@ def test_ospr_repeat_bit_identical_multichunk(n, monkeypatch):
     for r in runs[1:]:
         assert torch.equal(r.bits, runs[0].bits) and torch.equal(r.intensity, runs[0].intensity)
         assert torch.equal(r.mse, runs[0].mse)
+
+
+def test_grouped_column_pipeline_equals_plain():
+    """N = 2048 runs the column pass on the grouped pipeline (two consumer groups share one
+    TMA ring).  With the same transform code it must reproduce the plain
+    pipeline (HOLO_COL_G1=1, one group) bit for bit: holograms, intensity and MSE.  The plain
+    run happens in a subprocess because the variant is chosen once per process."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2004_04049_b200 as hb
+from holo_synth import LUT_SEED, Region, blobs_target
+n, S = 2048, 5
+T = torch.from_numpy(blobs_target(21, n, 16, 128.0, 320.0, Region.upper_half(n))).cuda()
+lut = hb.lut_generate(LUT_SEED, 10007)
+r = hb.ospr_generate(T, S, lut, phase_offset=77)
+torch.cuda.synchronize()
+np.savez(sys.argv[1], bits=r.bits.cpu().numpy(), inten=r.intensity.cpu().numpy(), mse=r.mse.cpu().numpy())
+""" % ROOT
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        for plain in (False, True):
+            env = dict(os.environ)
+            env.pop("HOLO_COL_G1", None)
+            if plain:
+                env["HOLO_COL_G1"] = "1"
+            f = os.path.join(d, f"r{int(plain)}.npz")
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=env, timeout=300)
+            out.append(np.load(f))
+    g, p = out
+    assert np.array_equal(g["bits"], p["bits"])
+    assert np.array_equal(g["inten"], p["inten"])
+    assert np.array_equal(g["mse"], p["mse"])
