@@ -265,6 +265,17 @@ def test_ospr_c3_full_parity(L):
     assert flips <= exempt
 
 
+@pytest.mark.parametrize("L,offset", [(1021, 0), (509, (1 << 33) + 12345), (1023, 777), (65537, 1 << 40)])
+def test_ospr_1024_non_degenerate_lengths(L, offset):
+    """Non-degenerate pool lengths at 1024^2 (L does not divide N^2, so every sub-frame draws
+    different phases), in the index modes the BASELINE lengths never reach at this size:
+    Lemire fast-mod below N (1021, 509, 1023) and a single wrap above it (65537), with
+    cursors beyond 2^32: every sub-frame's bits, conditional intensity and MSE."""
+    T = target_for(WORKLOADS["C3"])
+    _, flips, exempt = ospr_parity(T, 5, L, offset=offset)
+    assert flips <= exempt
+
+
 @pytest.mark.parametrize("L", [1 << 8, 1 << 12, 1 << 20])
 def test_ospr_c3_sampled_and_degenerate(L):
     """The other C3 lengths all divide N^2 (pin c3 #13), so every sub-frame draws the
