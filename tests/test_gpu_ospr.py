@@ -265,14 +265,15 @@ def test_ospr_c3_full_parity(L):
     assert flips <= exempt
 
 
-@pytest.mark.parametrize("L,offset", [(1021, 0), (509, (1 << 33) + 12345), (1023, 777), (65537, 1 << 40)])
-def test_ospr_1024_non_degenerate_lengths(L, offset):
+@pytest.mark.parametrize("L,offset,S", [(1021, 0, 5), (509, (1 << 33) + 12345, 5), (1023, 777, 5), (65537, 1 << 40, 5),
+                                        (1021, 3, 1), (1021, 3, 2)])   # one unpaired sub-frame; one pair
+def test_ospr_1024_non_degenerate_lengths(L, offset, S):
     """Non-degenerate pool lengths at 1024^2 (L does not divide N^2, so every sub-frame draws
     different phases), in the index modes the BASELINE lengths never reach at this size:
     Lemire fast-mod below N (1021, 509, 1023) and a single wrap above it (65537), with
     cursors beyond 2^32: every sub-frame's bits, conditional intensity and MSE."""
     T = target_for(WORKLOADS["C3"])
-    _, flips, exempt = ospr_parity(T, 5, L, offset=offset)
+    _, flips, exempt = ospr_parity(T, S, L, offset=offset)
     assert flips <= exempt
 
 
