@@ -743,13 +743,7 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
     float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RC::SLOT);
     float *sA = reinterpret_cast<float *>(smem_raw + RC::SA);           // [2][N]: A of ya, yb
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + RC::SA + 2 * (size_t)N * sizeof(float)) + warp;
-    // T of both rows (inputs, not produced by the previous pass), in flight during the transforms
-    float ta[PER], tb[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        ta[j] = __ldg(T + (size_t)ya * N + threadIdx.x + RC::THREADS * j);
-        tb[j] = __ldg(T + (size_t)yb * N + threadIdx.x + RC::THREADS * j);
-    }
+    // T of both rows: read in the epilogue (no registers held across the transforms)
     const int hp = (npairs + 1) / 2, p0 = half * hp, p1 = half ? npairs : hp;
     auto src = [&](int p) { return buf + ((size_t)p * N + (size_t)y) * N; };
     if (lane == 0) {
@@ -806,6 +800,12 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
     }
     __syncthreads();
     // a7: symmetrise both rows, write the mean intensity, fp64 MSE partials (R-12) over Omega
+    float ta[PER], tb[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        ta[j] = __ldg(T + (size_t)ya * N + threadIdx.x + RC::THREADS * j);
+        tb[j] = __ldg(T + (size_t)yb * N + threadIdx.x + RC::THREADS * j);
+    }
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const float *A0 = sA, *A1 = sA + N;
 #pragma unroll
