@@ -38,17 +38,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile every translation unit and link libholo.so (``out``; ``extra`` nvcc flags are
+    for experiment variants built next to the product library, e.g. -DHOLO_GS_NORM=0)."""
+    if not force and not extra and out == LIB and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if out == LIB else "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log" if out == LIB else os.path.basename(out) + ".build.log")
 
     def compile_one(tu):
         obj = os.path.join(objdir, tu.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, tu), "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, tu), "-o", obj]
         return cmd, subprocess.run(cmd, capture_output=True, text=True), obj
 
     with ThreadPoolExecutor(max_workers=len(TUS)) as ex:
@@ -60,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if res.returncode != 0:
             sys.stderr.write(res.stderr[-8000:])
             raise RuntimeError(f"nvcc failed (see {log})")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            *[obj for _, _, obj in results], "-o", tmp, "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -70,9 +72,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for _, r, _ in results:
             sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    a = sys.argv[1:]
+    o = a[a.index("--out") + 1] if "--out" in a else LIB
+    ex = [x for x in a if x.startswith("-D")]
+    print(build(force="--force" in a, verbose="-v" in a, out=os.path.abspath(o), extra=ex))

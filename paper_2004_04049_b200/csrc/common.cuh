@@ -174,6 +174,9 @@ __device__ __forceinline__ float rsqrt_sfu(float x)
 }
 constexpr float kFltMin = 1.17549435082228750797e-38f;   // smallest normal fp32
 
+// 1/sqrt(x), IEEE round-to-nearest (correctly rounded; the SFU estimate plus a Newton fix-up).
+__device__ __forceinline__ float rsqrt_rn(float x) { return __frsqrt_rn(x); }
+
 // ---- cyclic LUT index (step a1) ----------------------------------------------------------
 // idx = (rowbase + x) mod L for rowbase < L, x < N, evaluated per pixel without a
 // hardware divide: L >= N needs at most one subtraction; a power-of-two L is a mask;

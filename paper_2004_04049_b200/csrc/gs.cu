@@ -7,8 +7,10 @@
 //   gs_cols       column IFFT -> H_k; g2 constraint (H/|H| or nearest of Q levels);
 //                 last iteration writes h / level outputs; column FFT -> state.
 //   gs_rows       row FFT -> R'_k (x 1/N); g4: I_k = |R'_k|^2, fp64 partial sums of
-//                 I, I^2, I T^2 over Omega and (|R'_k| - T)^2 over the plane;
-//                 g5: R_k = T R'_k/|R'_k|; row IFFT -> state (or R_k / I_k outputs).
+//                 I, I^2, d^2, d I (d = a0 I - T^2) over Omega and (|R'_k| - T)^2 over
+//                 the plane; g5: R_k = T R'_k/|R'_k|; row IFFT -> state (or R_k / I_k).
+//                 The warp finishing a frame's last row item reduces the frame's item
+//                 partials in a fixed order -> MSE_k (R-12), E_k (ticket per frame).
 //
 // The 1/sqrt(N) factors of the inverse transforms are dropped: the constraint
 // and the amplitude replacement are invariant to a positive scale.
@@ -17,6 +19,7 @@
 namespace holo {
 
 constexpr int kMaxGroup = 64;
+constexpr int kGsParts = 5;   // per-item metric partial sums (gs_rows_kernel)
 
 template <int N>
 struct GsRowCfg {
@@ -26,7 +29,7 @@ struct GsRowCfg {
 
 __device__ __forceinline__ void block_reduce_n(double *s, int nvals, double *dst)
 {
-    __shared__ double red[32][4];
+    __shared__ double red[32][kGsParts];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = 0; i < nvals; ++i) {
         double x = s[i];
@@ -53,6 +56,39 @@ __device__ __forceinline__ void block_reduce_n(double *s, int nvals, double *dst
 __device__ __forceinline__ bool in_region(int y, int x, const holo_region &om)
 {
     return y >= om.row0 && y < om.row1 && x >= om.col0 && x < om.col1;
+}
+
+// The normalisations of g2 (H / |H|) and g5 (T R' / |R'|, |R'|).  HOLO_GS_NORM selects the
+// reciprocal square root: 0 = the SFU estimate (rel. error < 2^-22; default), 1 = correctly
+// rounded (__frsqrt_rn) then RN products, 2 = RN sqrt then RN divisions.  Measured at C4
+// (tools/gs_drift.py, profiles/r02_gs_drift.json): the 50-iteration MSE trajectory and the
+// one-step error are the same for all three (the fp32 transforms' rounding dominates), while
+// 1 and 2 slow the GS passes by 40-50 %, so the default is 0 (R-22).
+#ifndef HOLO_GS_NORM
+#define HOLO_GS_NORM 0
+#endif
+__device__ __forceinline__ float2 gs_unit(float2 h, float m2)
+{
+#if HOLO_GS_NORM == 2
+    const float s = __fsqrt_rn(m2);
+    return make_float2(__fdiv_rn(h.x, s), __fdiv_rn(h.y, s));
+#else
+    return f2::mul(h, f2::bc(HOLO_GS_NORM == 0 ? rsqrt_sfu(m2) : rsqrt_rn(m2)));
+#endif
+}
+// |X| and T / |X| for m2 = |X|^2 (both 0 when m2 is below the smallest normal: R-16's zero case).
+struct GsAmp {
+    float mag, g;
+};
+__device__ __forceinline__ GsAmp gs_amp(float m2, float tt, bool nz)
+{
+#if HOLO_GS_NORM == 2
+    const float s = nz ? __fsqrt_rn(m2) : 0.0f;
+    return GsAmp{s, nz ? __fdiv_rn(tt, s) : 0.0f};
+#else
+    const float rr = nz ? (HOLO_GS_NORM == 0 ? rsqrt_sfu(m2) : rsqrt_rn(m2)) : 0.0f;
+    return GsAmp{__fmul_rn(m2, rr), __fmul_rn(tt, rr)};
+#endif
 }
 
 // ---- g0: R_0 = T * lut[(base_b + p) mod L] (or a given R_in) -> state; T sums over Omega -----------
@@ -100,12 +136,59 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
     block_reduce_n(s, 2, tparts + ((size_t)fr * kGsTBlocks + blockIdx.x) * 2);
 }
 
+// g4 of iteration k for the frames of a launch group (pointers offset to the group).
+struct GsMetrics {
+    const float *a0;      // [G] prior a0 = sum_Omega T^2 / |Omega| (gs_tsum_kernel)
+    const double *tsum;   // [G][2] sum_Omega T^2, T^4
+    const double *parts;  // [G][nblk][kGsParts] the row pass's item partial sums
+    double *mse, *err_e;  // [G][iters] outputs (nullable)
+    int nframes, nblk, iters, k;
+    double inv_count;     // 1 / |Omega|
+};
+
+// R-12 for frame fr from its item partials, reduced in a fixed order by the whole CTA: a =
+// S_T2 / S_I and, about the prior a0 the partials were taken at (d = a0 I - T^2),
+//   sum (a I - T^2)^2 = S_dd + 2 (a - a0) S_dI + (a - a0)^2 S_II;   S_I = 0: a = 0, sum = S_T4.
+__device__ __forceinline__ void gs_frame_metrics(const GsMetrics &gm, int fr)
+{
+    const double *pp = gm.parts + (size_t)fr * gm.nblk * kGsParts;
+    double s[kGsParts] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < gm.nblk; i += blockDim.x)
+#pragma unroll
+        for (int j = 0; j < kGsParts; ++j)
+            s[j] += pp[(size_t)i * kGsParts + j];
+    __shared__ double o[kGsParts];
+    block_reduce_n(s, kGsParts, o);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double sT2 = gm.tsum[2 * fr], sT4 = gm.tsum[2 * fr + 1];
+        double sum = sT4;
+        if (o[0] != 0.0) {
+            const double da = sT2 / o[0] - (double)gm.a0[fr];
+            sum = o[2] + 2.0 * da * o[3] + da * da * o[1];
+        }
+        if (gm.mse)
+            gm.mse[(size_t)fr * gm.iters + gm.k] = (sum > 0.0 ? sum : 0.0) * gm.inv_count;
+        if (gm.err_e)
+            gm.err_e[(size_t)fr * gm.iters + gm.k] = o[4];
+    }
+}
+
+// The last iteration's metrics (earlier ones are reduced in the next column pass's prologue).
+__global__ void __launch_bounds__(256)
+gs_mse_kernel(const GsMetrics gm)
+{
+    HOLO_PDL_ENTRY();
+    gs_frame_metrics(gm, blockIdx.x);
+}
+
 // ---- column pass: IFFT -> constraint -> FFT (TMA-fed pipeline) ----------------------------------
 template <int N, bool QUANT>
 struct GsColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     static constexpr int kWidth = 8;   // columns per tile (4 measured 6 % slower for this body)
     static constexpr int kGroups = 1;
+    static constexpr bool kPrologue = true;
     struct Args {
         const float2 *tw;
         float2 *buf;          // the group's state (updated in place)
@@ -113,7 +196,20 @@ struct GsColBody {
         const float2 *qtab;   // Q-entry level table (QUANT only)
         float2 *holo;
         uint8_t *lev;
+        GsMetrics pend;       // metrics of the previous row pass to reduce (pend.parts NULL: none)
     };
+    // The previous iteration's per-frame metric reductions go to the CTAs that own one tile
+    // fewer than the others (ntiles mod grid of them own one more), so they add nothing to the
+    // pass's critical path; the reductions overlap the CTAs' first TMA tile loads.
+    static __device__ __forceinline__ void prologue(const Args &a, int ntiles)
+    {
+        if (a.pend.parts == nullptr)
+            return;
+        const int rem = ntiles % (int)gridDim.x;
+        for (int fr = ((int)blockIdx.x + (int)gridDim.x - rem) % (int)gridDim.x; fr < a.pend.nframes;
+             fr += (int)gridDim.x)
+            gs_frame_metrics(a.pend, fr);
+    }
     template <class F, int W>
     static __device__ __forceinline__ void run(float2 (&v)[F::E], float2 *sm, uint32_t *, int c, int t, int fr,
                                                int tile,
@@ -138,7 +234,7 @@ struct GsColBody {
                 if constexpr (!QUANT) {
                     const float m2 = __fmaf_rn(hk.x, hk.x, __fmul_rn(hk.y, hk.y));
                     o = m2 < kFltMin ? make_float2(1.0f, 0.0f)               // R-16: H = 0 -> +1
-                                     : f2::mul(hk, f2::bc(rsqrt_sfu(m2)));   // H / |H|
+                                     : gs_unit(hk, m2);                      // H / |H|
                 } else {
                     float th = atan2f(hk.y, hk.x);
                     if (th < 0.0f)
@@ -184,13 +280,14 @@ __global__ void gs_qtab_kernel(int levels, float2 *__restrict__ qtab)
 enum GsRowMode : int { GS_FUSED = 0, GS_LAST = 1, GS_STEP = 2 };
 
 // Items are GPW-row groups of the group's frames (NGRP = N / GPW per frame); each item's
-// fp64 partial sums (I, I^2, I T^2 over Omega; (|R'| - T)^2 over the plane) go to
-// parts[frame * frame_stride + grp * 4] for a fixed-order reduction by gs_mse_kernel.
+// fp64 partial sums (I, I^2, d^2, d I over Omega with d = a0 I - T^2; (|R'| - T)^2 over the
+// plane) go to parts[frame][grp] for a fixed-order reduction in the next column pass's
+// prologue (GsColBody::prologue), or by gs_mse_kernel after the last iteration.
 template <int N, int MODE>
 __global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
 gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__restrict__ T, int nitems, holo_region om,
-               float *__restrict__ inten, float2 *__restrict__ r_out, double *__restrict__ parts,
-               size_t frame_stride_parts)
+               float *__restrict__ inten, float2 *__restrict__ r_out, const float *__restrict__ a0,
+               double *__restrict__ parts)
 {
     HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
@@ -208,6 +305,11 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
     fft::Twiddles<N, false> twr;                          // pool twiddles (register budget)
     twr.load(tw, t);
     constexpr float inv_n = 1.0f / (float)N;                 // exact power of two
+    static_assert(E <= 64, "one column-mask bit per element");
+    uint64_t colmask = 0;                                     // bit r: column t + R1 r lies in Omega
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        colmask |= (uint64_t)(t + R1 * r >= om.col0 && t + R1 * r < om.col1) << r;
     #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int k = 0; item < nitems; item += stride, ++k) {
         const int s = k & 1;
@@ -225,7 +327,6 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = sl[g * N + t + R1 * m];
-        double sums[4] = {0.0, 0.0, 0.0, 0.0};
         // forward FFT, then (FUSED) the inverse through the same transform body:
         // F^-1{x} = conj(F{conj(x)}) exactly (instruction cache: one copy of the FFT code)
 #pragma unroll 1
@@ -245,42 +346,47 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                     state[rofs + t + R1 * r] = v[r];
                 break;
             }
-            // g4 metrics: fp32 partial sums over this thread's E elements (unbiased rounding, a
-            // relative error ~1e-7 per partial), then fp64 across lanes, rows and frames
-            float fe = 0.0f, sI = 0.0f, sII = 0.0f, sIT = 0.0f;
-            const bool row_in = y >= om.row0 && y < om.row1, all_cols = om.col0 == 0 && om.col1 >= N;
+            // g4 metrics.  R-12 needs sum (a I - T^2)^2 with a = sum T^2 / sum I, known only after
+            // the pass; it is accumulated about the frame's prior a0 = sum_Omega T^2 / |Omega| (for
+            // the full plane this IS a, by Parseval: sum I = sum |h|^2 = N^2) as
+            //   sum (a I - T^2)^2 = S_dd + 2 (a - a0) S_dI + (a - a0)^2 S_II,  d = a0 I - T^2,
+            // so no large terms cancel (gs_frame_metrics).  fp32 partial sums over this thread's E
+            // elements (all terms of S_dd, S_II positive), then fp64 across lanes, rows, frames.
+            // The sums run on m2 = |X|^2 = N^2 I (I = m2 / N^2 is an exact power-of-two scaling, so
+            // sum m2 / N^2 is bit-identical to sum I); the scales are applied in fp64 afterwards.
+            float fe = 0.0f, sI = 0.0f, sII = 0.0f, sDD = 0.0f, sDI = 0.0f;
+            const float a0n = __fmul_rn(a0[fr], inv_n * inv_n);       // a0 / N^2 (exact)
+            const uint64_t in_om = (y >= om.row0 && y < om.row1) ? colmask : 0u;   // bit r: x in Omega
 #pragma unroll
             for (int r = 0; r < E; ++r) {
                 const int x = t + R1 * r;
                 const float2 X = v[r];
                 // explicit rounding: identical arithmetic in every instantiation (fused == step)
                 const float m2 = __fmaf_rn(X.x, X.x, __fmul_rn(X.y, X.y));
-                const float I = __fmul_rn(m2, inv_n * inv_n);
                 const bool nz = m2 >= kFltMin;
-                const float rr = nz ? rsqrt_sfu(m2) : 0.0f;
-                const float amp = __fmul_rn(__fmul_rn(m2, rr), inv_n);   // |R'_k|
                 const float tt = tv[r];
-                const float d = __fsub_rn(amp, tt);
+                const GsAmp ga = gs_amp(m2, tt, nz);
+                const float d = __fmaf_rn(ga.mag, inv_n, -tt);              // |R'_k| - T
                 fe = __fmaf_rn(d, d, fe);
-                if (row_in && (all_cols || (x >= om.col0 && x < om.col1))) {
-                    sI = __fadd_rn(sI, I);
-                    sII = __fmaf_rn(I, I, sII);
-                    sIT = __fmaf_rn(I, __fmul_rn(tt, tt), sIT);
+                if ((in_om >> r) & 1u) {
+                    const float dd = __fmaf_rn(a0n, m2, -__fmul_rn(tt, tt));   // a0 I - T^2
+                    sI = __fadd_rn(sI, m2);
+                    sII = __fmaf_rn(m2, m2, sII);
+                    sDD = __fmaf_rn(dd, dd, sDD);
+                    sDI = __fmaf_rn(dd, m2, sDI);
                 }
                 if (MODE == GS_LAST || MODE == GS_STEP) {
                     if (inten != nullptr)
-                        inten[rofs + x] = I;
+                        inten[rofs + x] = __fmul_rn(m2, inv_n * inv_n);
                 }
                 if (MODE != GS_LAST)   // conj(R_k), R_k = T X / |X| (R-16: |R'| = 0 -> T)
-                    v[r] = nz ? f2::mul(conjf2(X), f2::bc(__fmul_rn(tt, rr))) : make_float2(tt, -0.0f);
+                    v[r] = nz ? f2::mul(conjf2(X), f2::bc(ga.g)) : make_float2(tt, -0.0f);
             }
-            sums[0] = (double)sI;
-            sums[1] = (double)sII;
-            sums[2] = (double)sIT;
-            sums[3] = (double)fe;
+            constexpr double i2 = 1.0 / ((double)N * N), i4 = i2 * i2;   // exact
+            double sums[kGsParts] = {(double)sI * i2, (double)sII * i4, (double)sDD, (double)sDI * i2, (double)fe};
             // warp reduction of the item's sums (lanes of all GPW rows of the item)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < kGsParts; ++i) {
                 double x = sums[i];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
@@ -288,11 +394,10 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
                 sums[i] = x;
             }
             if (lane == 0) {
-                double *dst = parts + (size_t)fr * frame_stride_parts + (size_t)grp * 4;
-                dst[0] = sums[0];
-                dst[1] = sums[1];
-                dst[2] = sums[2];
-                dst[3] = sums[3];
+                double *dst = parts + ((size_t)fr * NGRP + grp) * kGsParts;
+#pragma unroll
+                for (int i = 0; i < kGsParts; ++i)
+                    dst[i] = sums[i];
             }
             if (MODE == GS_STEP) {
 #pragma unroll
@@ -305,37 +410,23 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
     }
 }
 
-// One CTA per (frame, iteration): fixed-order sums -> MSE (R-12) and E.
-__global__ void __launch_bounds__(128)
-gs_mse_kernel(const double *__restrict__ parts, const double *__restrict__ tparts, int nblk, int iters,
-              double inv_count, double *__restrict__ mse, double *__restrict__ err_e)
+// One CTA per frame of a launch group: fixed-order sum of the prepare kernel's T partials ->
+// tsum[frame] = (sum T^2, sum T^4) over Omega and the prior a0 = sum T^2 / |Omega| that the
+// row pass takes its metric partials about (exactly R-12's a for the full plane, by Parseval).
+__global__ void __launch_bounds__(kGsTBlocks)
+gs_tsum_kernel(const double *__restrict__ tparts, double inv_count, double *__restrict__ tsum, float *__restrict__ a0)
 {
     HOLO_PDL_ENTRY();
-    const int b = blockIdx.x / iters;
-    const double *p = parts + (size_t)blockIdx.x * nblk * 4;
-    const double *q = tparts + (size_t)b * kGsTBlocks * 2;
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
-    double u[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x)
-        for (int k = 0; k < 4; ++k)
-            s[k] += p[(size_t)i * 4 + k];
-    for (int i = threadIdx.x; i < kGsTBlocks; i += blockDim.x) {
-        u[0] += q[(size_t)i * 2];
-        u[1] += q[(size_t)i * 2 + 1];
-    }
-    __shared__ double o1[4];
-    __shared__ double o2[4];
-    block_reduce_n(s, 4, o1);
-    __syncthreads();
-    block_reduce_n(u, 2, o2);
+    const int fr = blockIdx.x;
+    const double *q = tparts + ((size_t)fr * kGsTBlocks + threadIdx.x) * 2;
+    double u[2] = {q[0], q[1]};
+    __shared__ double o[2];
+    block_reduce_n(u, 2, o);
     __syncthreads();
     if (threadIdx.x == 0) {
-        const double a = o1[0] == 0.0 ? 0.0 : o2[0] / o1[0];
-        const double sum = a * a * o1[1] - 2.0 * a * o1[2] + o2[1];
-        if (mse)
-            mse[blockIdx.x] = (sum > 0.0 ? sum : 0.0) * inv_count;
-        if (err_e)
-            err_e[blockIdx.x] = o1[3];
+        tsum[2 * fr] = o[0];
+        tsum[2 * fr + 1] = o[1];
+        a0[fr] = (float)(o[0] * inv_count);
     }
 }
 
@@ -375,11 +466,13 @@ static int gs_nblk(int n)
 struct GsWs {
     float2 *qtab;
     float2 *state;
-    double *parts;
-    double *tparts;
+    double *parts;    // [G][NBLK][kGsParts] row-pass item partials of the current iteration
+    double *tparts;   // [G][kGsTBlocks][2] prepare-kernel partials of sum T^2, T^4
+    double *tsum;     // [G][2]
+    float *a0;        // [G]
 };
 
-static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
+static size_t gs_ws_layout(int n, int batch, char *base, GsWs *w)
 {
     const size_t P = (size_t)n * n;
     const int G = gs_group(n, batch), nblk = gs_nblk(n);
@@ -389,14 +482,21 @@ static size_t gs_ws_layout(int n, int batch, int iters, char *base, GsWs *w)
     const size_t o_state = off;
     off = al256(off + (size_t)G * P * sizeof(float2));
     const size_t o_parts = off;
-    off = al256(off + (size_t)batch * iters * nblk * 4 * sizeof(double));
+    off = al256(off + (size_t)G * nblk * kGsParts * sizeof(double));
     const size_t o_tparts = off;
-    off = al256(off + (size_t)batch * kGsTBlocks * 2 * sizeof(double));
+    off = al256(off + (size_t)G * kGsTBlocks * 2 * sizeof(double));
+    const size_t o_tsum = off;
+    off = al256(off + (size_t)G * 2 * sizeof(double));
+    const size_t o_a0 = off;
+    off = al256(off + (size_t)G * sizeof(float));
+
     if (w) {
         w->qtab = (float2 *)(base + o_qtab);
         w->state = (float2 *)(base + o_state);
         w->parts = (double *)(base + o_parts);
         w->tparts = (double *)(base + o_tparts);
+        w->tsum = (double *)(base + o_tsum);
+        w->a0 = (float *)(base + o_a0);
     }
     return off;
 }
@@ -413,15 +513,14 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                           uint8_t *holo_levels, float *intensity, double *mse, double *err_e, holo_region om,
                           void *ws, cudaStream_t s)
 {
-    using RC = GsRowCfg<N>;
     constexpr size_t P = (size_t)N * N;
     GsWs w;
-    gs_ws_layout(N, batch, iters, (char *)ws, &w);
+    gs_ws_layout(N, batch, (char *)ws, &w);
     const int G = gs_group(N, batch);
     const LutIndexer ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, N);
     const uint32_t off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
     const uint32_t p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
-    const size_t pstride = (size_t)iters * RC::NBLK * 4;   // parts per frame
+    const double inv_cnt = 1.0 / ((double)(om.row1 - om.row0) * (double)(om.col1 - om.col0));
     if (levels > 0)
         HOLO_TRY(launch(K_GS_COLS, gs_qtab_kernel, dim3((levels + 255) / 256), dim3(256), 0, s, levels, w.qtab));
     for (int g0 = 0; g0 < batch; g0 += G) {
@@ -429,45 +528,54 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
         HOLO_TRY(launch(K_GS_ROWS_INIT, gs_prepare_kernel<N>, dim3(kGsTBlocks, ng), dim3(256), 0, s,
                         target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
                         r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state,
-                        w.tparts + (size_t)g0 * kGsTBlocks * 2));
+                        w.tparts));
+        HOLO_TRY(launch(K_MSE_REDUCE, gs_tsum_kernel, dim3(ng), dim3(kGsTBlocks), 0, s, (const double *)w.tparts,
+                        inv_cnt, w.tsum, w.a0));
         HOLO_TRY((launch_rows_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));   // F{conj(R_0)}
+        using RP = RowPipe<N>;
+        const float *Tg = target + g0 * P;
+        GsMetrics gm{w.a0, w.tsum, w.parts, mse ? mse + (size_t)g0 * iters : (double *)nullptr,
+                     err_e ? err_e + (size_t)g0 * iters : (double *)nullptr, ng, GsRowCfg<N>::NBLK, iters, 0, inv_cnt};
+        const bool metrics = mse != nullptr || err_e != nullptr;
         for (int k = 0; k < iters; ++k) {
             const bool last = (k == iters - 1);
+            GsMetrics pend = gm;              // iteration k-1's partials, reduced in this pass's prologue
+            pend.k = k - 1;
+            if (k == 0 || !metrics)
+                pend.parts = nullptr;
             if (levels == 0) {
                 typename GsColBody<N, false>::Args ca{tw, w.state, 0, nullptr,
-                                                      (last && holo) ? holo + g0 * P : (float2 *)nullptr, nullptr};
+                                                      (last && holo) ? holo + g0 * P : (float2 *)nullptr, nullptr, pend};
                 HOLO_TRY((launch_cols<N, GsColBody<N, false>>(K_GS_COLS, w.state, ng, ca, s)));
             } else {
                 typename GsColBody<N, true>::Args ca{tw, w.state, levels, w.qtab,
                                                      (last && holo) ? holo + g0 * P : (float2 *)nullptr,
-                                                     (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr};
+                                                     (last && holo_levels) ? holo_levels + g0 * P : (uint8_t *)nullptr,
+                                                     pend};
                 HOLO_TRY((launch_cols<N, GsColBody<N, true>>(K_GS_COLS, w.state, ng, ca, s)));
             }
-            double *pk = w.parts + (size_t)g0 * pstride + (size_t)k * RC::NBLK * 4;
-            const float *Tg = target + g0 * P;
-            using RP = RowPipe<N>;
             constexpr size_t smem = ring_smem<RP::SLOT_C, RP::WPC>();
-            const int nitems = ng * (N / RP::GPW);
+            const int nitems = ng * GsRowCfg<N>::NBLK;
             float *ig = intensity ? intensity + g0 * P : (float *)nullptr;
+            const float *a0 = w.a0;
             if (r_out != nullptr) {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_STEP>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, ig, r_out + g0 * P, pk, pstride));
+                                w.state, Tg, nitems, om, ig, r_out + g0 * P, a0, w.parts));
             } else if (last) {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_LAST>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_LAST>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, ig, (float2 *)nullptr, pk, pstride));
+                                w.state, Tg, nitems, om, ig, (float2 *)nullptr, a0, w.parts));
             } else {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_FUSED>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, pk, pstride));
+                                w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, a0, w.parts));
             }
         }
-    }
-    if (mse || err_e) {
-        const double cnt = (double)(om.row1 - om.row0) * (double)(om.col1 - om.col0);
-        HOLO_TRY(launch(K_MSE_REDUCE, gs_mse_kernel, dim3(batch * iters), dim3(128), 0, s,
-                        (const double *)w.parts, (const double *)w.tparts, RC::NBLK, iters, 1.0 / cnt, mse, err_e));
+        if (metrics) {
+            gm.k = iters - 1;
+            HOLO_TRY(launch(K_MSE_REDUCE, gs_mse_kernel, dim3(ng), dim3(256), 0, s, (const GsMetrics)gm));
+        }
     }
     return HOLO_OK;
 }
@@ -504,7 +612,8 @@ extern "C" size_t holo_gs_workspace_size(int32_t n, int32_t batch, int32_t iters
 {
     if (check_n(n) != HOLO_OK || batch < 1 || iters < 1)
         return 0;
-    return gs_ws_layout(n, batch, iters, nullptr, nullptr);
+    (void)iters;
+    return gs_ws_layout(n, batch, nullptr, nullptr);
 }
 
 static holo_status gs_check_common(const float *target, int32_t n, int32_t batch, int32_t levels, holo_region om,

@@ -18,7 +18,18 @@
 
 #include <stdlib.h>
 
+#include <type_traits>
+
 namespace holo {
+
+// A column-pipeline body may declare `static constexpr bool kPrologue = true` and a
+// `prologue(args, ntiles)` that every thread of every CTA runs once, after the CTA's first
+// tile loads are issued (so that work overlaps them).  GS reduces the previous row pass's
+// metric partials there.
+template <class B, class = void>
+struct HasPrologue : std::false_type {};
+template <class B>
+struct HasPrologue<B, std::void_t<decltype(B::kPrologue)>> : std::integral_constant<bool, B::kPrologue> {};
 
 // ---- row pipeline ---------------------------------------------------------------------------
 // Warp-persistent, per-warp double-buffered: a work item is GPW = 32/T consecutive rows
@@ -208,6 +219,8 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
             if (tile < ntiles)
                 issue(tile, j % S);
         }
+    if constexpr (HasPrologue<Body>::value)
+        Body::prologue(a, ntiles);
     int k = 0;
     #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
@@ -301,6 +314,8 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
             if (tile < ntiles)
                 issue(tile, j);
         }
+    if constexpr (HasPrologue<Body>::value)
+        Body::prologue(a, ntiles);
     #pragma unroll 1   // one copy of the transform code (instruction cache)
     for (int k = g, tile = blockIdx.x + g * gridDim.x; tile < ntiles; k += 2, tile += 2 * gridDim.x) {
         const int s = k % S;
