@@ -47,6 +47,29 @@ def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
     return t
 
 
+def _need_out(t: Optional[torch.Tensor], dtype: torch.dtype, shape: Tuple[int, ...], dev: torch.device,
+              name: str) -> Optional[torch.Tensor]:
+    """A caller-supplied output must match what the ABI will write through its raw pointer
+    (dtype, exact shape, device, contiguity): the library cannot check a device buffer's size."""
+    if t is None:
+        return None
+    _need(t, dtype, name)
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.device != dev:
+        raise ValueError(f"{name} must be on {dev}, got {t.device}")
+    return t
+
+
+def _workspace(ws: Optional[torch.Tensor], need: int, dev: torch.device) -> torch.Tensor:
+    if ws is None or ws.numel() < need:
+        return torch.empty(need, dtype=torch.uint8, device=dev)
+    _need(ws, torch.uint8, "workspace")
+    if ws.device != dev:
+        raise ValueError(f"workspace must be on {dev}, got {ws.device}")
+    return ws
+
+
 def default_omega(n: int, algo: str) -> Tuple[int, int, int, int]:
     """R-13: OSPR measures rows [1, N/2) x all columns; GS the full plane."""
     return (1, n // 2, 0, n) if algo == "ospr" else (0, n, 0, n)
@@ -71,6 +94,8 @@ def lut_generate(seed: int, n_lut: int, device=None, out: Optional[torch.Tensor]
     if out is None:
         out = torch.empty(n_lut, dtype=torch.complex64, device=dev)
     _need(out, torch.complex64, "out")
+    if out.numel() != n_lut:
+        raise ValueError(f"out must hold n_lut = {n_lut} entries, got {out.numel()}")
     check(lib().holo_lut_generate(seed & 0xFFFFFFFFFFFFFFFF, n_lut, out.data_ptr(), _stream(out.device)))
     return out
 
@@ -116,9 +141,13 @@ def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] 
             bits=torch.empty((F, e - b, n, n // 8), dtype=torch.uint8, device=dev) if want_bits else None,
             intensity=torch.empty((F, n, n), dtype=torch.float32, device=dev),
             mse=torch.empty(F, dtype=torch.float64, device=dev) if (want_mse and full) else None)
-    need = ospr_workspace_bytes(n, F, n_sub)
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    else:
+        _need_out(out.bits, torch.uint8, (F, e - b, n, n // 8), dev, "out.bits")
+        if out.intensity is None:
+            raise ValueError("out.intensity is required")
+        _need_out(out.intensity, torch.float32, (F, n, n), dev, "out.intensity")
+        _need_out(out.mse, torch.float64, (F,), dev, "out.mse")
+    workspace = _workspace(workspace, ospr_workspace_bytes(n, F, n_sub), dev)
     if prng_seed is not None:
         if lut is not None:
             raise ValueError("pass either lut or prng_seed, not both")
@@ -144,12 +173,11 @@ def ospr_finalize(target: torch.Tensor, intensity_sum: torch.Tensor, n_sub: int,
     t3 = target if target.dim() == 3 else target.unsqueeze(0)
     F, n, _ = t3.shape
     om = omega if omega is not None else default_omega(n, "ospr")
-    out = torch.empty_like(intensity_sum) if out is None else out
-    mse = (mse_out if mse_out is not None else torch.empty(F, dtype=torch.float64, device=t3.device)) \
-        if want_mse else None
-    need = int(lib().holo_ospr_finalize_workspace_size())
-    ws = workspace if workspace is not None and workspace.numel() >= need else \
-        torch.empty(need, dtype=torch.uint8, device=t3.device)
+    _need_out(intensity_sum, torch.float32, (F, n, n), t3.device, "intensity_sum")
+    out = torch.empty_like(intensity_sum) if out is None else _need_out(out, torch.float32, (F, n, n), t3.device, "out")
+    mse = (_need_out(mse_out, torch.float64, (F,), t3.device, "mse_out") if mse_out is not None
+           else torch.empty(F, dtype=torch.float64, device=t3.device)) if want_mse else None
+    ws = _workspace(workspace, int(lib().holo_ospr_finalize_workspace_size()), t3.device)
     check(lib().holo_ospr_finalize(t3.data_ptr(), intensity_sum.data_ptr(), n, F, n_sub, _region(om),
                                    out.data_ptr(), _ptr(mse), ws.data_ptr(), ws.numel(), _stream(t3.device)))
     return out, mse
@@ -187,9 +215,13 @@ def gs_generate(target: torch.Tensor, iters: int, lut: Optional[torch.Tensor] = 
             intensity=torch.empty((B, n, n), dtype=torch.float32, device=dev) if want_intensity else None,
             mse=torch.empty((B, iters), dtype=torch.float64, device=dev) if want_mse else None,
             err_e=torch.empty((B, iters), dtype=torch.float64, device=dev) if want_err else None)
-    need = gs_workspace_bytes(n, B, iters)
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    else:
+        _need_out(out.holo, torch.complex64, (B, n, n), dev, "out.holo")
+        _need_out(out.levels, torch.uint8, (B, n, n), dev, "out.levels")
+        _need_out(out.intensity, torch.float32, (B, n, n), dev, "out.intensity")
+        _need_out(out.mse, torch.float64, (B, iters), dev, "out.mse")
+        _need_out(out.err_e, torch.float64, (B, iters), dev, "out.err_e")
+    workspace = _workspace(workspace, gs_workspace_bytes(n, B, iters), dev)
     lp, L = _lut_args(lut)
     check(lib().holo_gs_generate(t3.data_ptr(), n, B, iters, lp, L, phase_offset, levels, _ptr(out.holo),
                                  _ptr(out.levels), _ptr(out.intensity), _ptr(out.mse), _ptr(out.err_e),
@@ -227,7 +259,7 @@ def fft2(x: torch.Tensor, inverse: bool = False, out: Optional[torch.Tensor] = N
     _need(x, torch.complex64, "x")
     x3 = x if x.dim() == 3 else x.unsqueeze(0)
     B, n, _ = x3.shape
-    out = torch.empty_like(x3) if out is None else out
+    out = torch.empty_like(x3) if out is None else _need_out(out, torch.complex64, tuple(x3.shape), x3.device, "out")
     check(lib().holo_fft2(x3.data_ptr(), out.data_ptr(), n, B, int(inverse), _stream(x3.device)))
     return out if x.dim() == 3 else out[0]
 

@@ -251,6 +251,7 @@ __device__ __forceinline__ float2 lut_at(const float2 *__restrict__ lut, uint32_
 }
 
 // The one-entry pool {1 + 0i} standing for N_LUT = 0 (flat phase, R-6).
-static __device__ const float2 k_flat_lut[1] = {{1.0f, 0.0f}};
+// (16-byte aligned, two copies: pass A may stage it by a 16-byte bulk copy)
+static __device__ __align__(16) const float2 k_flat_lut[2] = {{1.0f, 0.0f}, {1.0f, 0.0f}};
 
 } // namespace holo

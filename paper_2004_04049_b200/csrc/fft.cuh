@@ -316,6 +316,35 @@ __device__ __forceinline__ void fft2pass(float2 (&v)[Plan<N>::E], float2 *sm, in
     fft2pass_impl<N, INV, IL, WS>(v, sm, t, TwGlobal<N>{twp + Plan<N>::TW_OFFSET + t});
 }
 
+// Pass-2 twiddles W_N^{r t} factorised as W_N^{8a t} * W_N^{b t} (r = 8a + b, b < 8): the
+// (R2/8 - 1) + 7 factors of role t are loaded from the pool once and kept in registers
+// (20 registers at N = 1024 instead of 62 for the full set); each twiddle with a, b > 0 costs
+// one complex multiply (one extra rounding, ~1 ulp) instead of a load per transform.
+template <int N>
+struct TwFact {
+    static constexpr int R1 = Plan<N>::R1, R2 = Plan<N>::R2, NA = (R2 + 7) / 8;
+    float2 lo[8], hi[NA];
+    __device__ __forceinline__ void load(const float2 *__restrict__ twp, int t)
+    {
+        const float2 *p = twp + Plan<N>::TW_OFFSET + t;
+#pragma unroll
+        for (int b = 1; b < 8 && b < R2; ++b)
+            lo[b] = __ldg(p + b * R1);
+#pragma unroll
+        for (int a = 1; a < NA; ++a)
+            hi[a] = __ldg(p + 8 * a * R1);
+    }
+    __device__ __forceinline__ float2 operator()(int r) const
+    {
+        const int a = r / 8, b = r % 8;
+        if (a == 0)
+            return lo[b];
+        if (b == 0)
+            return hi[a];
+        return cmul(hi[a], lo[b]);
+    }
+};
+
 // Twiddles from the pool, with a hook after the exchange (see fft2pass_impl).
 template <int N, bool INV, int IL, bool WS, class Hook>
 __device__ __forceinline__ void fft2pass_hook(float2 (&v)[Plan<N>::E], float2 *sm, int t, const float2 *__restrict__ twp,
