@@ -11,13 +11,23 @@ One step = one pass of every hot-path row of SURVEY.md §8(a) over one batch:
   (holograms, mean replay intensity, MSE), inputs resident in HBM.
   GS (`gs` block): BASELINE configs[3] (C4) -- 64 frames x 50 iterations at
   1024x1024, continuous phase-only, LUT 2^16.
+  C5 video (`c5_video` block): BASELINE configs[4] -- 2048^2 frames, N_SF = 32,
+  streamed back to back.
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier and
 torch.cuda.synchronize(); L2 is flushed (256 MiB write) before every timed step;
-CUDA events on the launching stream; max over ranks.  Multi-GPU (torchrun): OSPR
-sub-frames are sharded across ranks and the partial intensity sums are combined
-with an NCCL all-reduce before the MSE (strong scaling); GS frames are sharded
-(no collective).  `--impl reference` times the fp64 CPU oracle (oracle/) on the
-host cores on the same workload (the paper has no GPU implementation).
+CUDA events on the launching stream; max over ranks.
+Multi-GPU (torchrun, one process per GPU, NCCL):
+  * C3 headline (`--ospr-shard frames`, default): rank r runs its own frame set r
+    (global cursor, R-2) -- independent problems, no collective, weak scaling;
+    `--ospr-shard subframes` splits one frame set's sub-frames over the ranks
+    instead (reduce-scatter + a7 on the owned rows + 5-double all-reduce).
+  * C5 video: every frame's sub-frames are split over the ranks (configs[4]'s
+    partition); C-1 = NCCL reduce-scatter of the partial intensity (each rank owns
+    2048/N rows), a7 on the owned rows, C-2 = NCCL all-reduce of five doubles, then
+    the MSE, all on a side stream overlapping the next frame's passes.
+  * GS: the C4 frames are sharded (no collective).
+`--impl reference` times the fp64 CPU oracle (oracle/) on the host cores on the
+same workload (the paper has no GPU implementation).
 """
 from __future__ import annotations
 
@@ -259,8 +269,10 @@ def kernel_times(hb, step_fn, steps, flush, use_graph):
 
 
 def graphed_stages(pre, collective, post, enabled):
-    """A step made of two local parts around one collective: pre and post are each captured
-    into a CUDA graph (after one eager run), the collective (NCCL) runs eagerly between them."""
+    """A step made of local parts around one (eager) collective: pre and post (None: nothing)
+    are each captured into a CUDA graph (after one eager run), the collective (NCCL) runs
+    eagerly between them; a collective marked `.local` (nothing to exchange) is captured too."""
+    post = post or (lambda: None)
     if not enabled:
         def eager():
             pre()
@@ -280,17 +292,15 @@ def graphed_stages(pre, collective, post, enabled):
             post()
         torch.cuda.synchronize()
         return g.replay
-    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    g1 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g1):
         pre()
-    with torch.cuda.graph(g2):
-        post()
     torch.cuda.synchronize()
 
     def replay():
         g1.replay()
         collective()
-        g2.replay()
+        post()
     return replay
 
 
@@ -311,7 +321,7 @@ def run_gpu(args):
     w3 = WORKLOADS["C3"]
     n, S, P = w3.n, w3.n_sub, w3.n * w3.n
     T = torch.from_numpy(target_for(w3)).to(dev)
-    from paper_2004_04049_b200.parallel import shard_range
+    from paper_2004_04049_b200.parallel import shard_range, subframe_range  # noqa: F401
     # HOLO_BENCH_FAKE_WORLD=k (testing only, N = 1): run rank 0's shard of a k-way split with a
     # no-op collective, to exercise the N > 1 step structure (graphs around the collective)
     fake = int(os.environ.get("HOLO_BENCH_FAKE_WORLD", "0")) if world == 1 else 0
@@ -322,7 +332,7 @@ def run_gpu(args):
     sworld = 1 if frames_mode else (fake if fake > 1 else world)
     srank = 0 if frames_mode else rank
     frame_off = rank * S * P if frames_mode else 0
-    sb, se = shard_range(S, sworld, srank)
+    sb, se = subframe_range(S, sworld, srank)
     full = (sworld == 1)
     ws = torch.empty(hb.ospr_workspace_bytes(n, 1, S), dtype=torch.uint8, device=dev)
     lut_buf = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
@@ -332,26 +342,41 @@ def run_gpu(args):
     mse_buf = torch.empty(1, dtype=torch.float64, device=dev)
 
     from paper_2004_04049_b200.parallel import ShardedOspr
-    sharded = ShardedOspr(sworld, srank, all_reduce=(lambda t: None)) if fake > 1 else ShardedOspr(sworld, srank)
+    stand_in = dict(reduce_scatter=lambda o, i: o.copy_(i[:o.numel()]), all_reduce=lambda t: None)
+    sharded = ShardedOspr(sworld, srank, **(stand_in if fake > 1 else {}))
+    if not full:
+        r0, r1 = sharded.rows(n)
+        mean_rows = torch.empty((1, r1 - r0, n), dtype=torch.float32, device=dev)
+        sums_buf = torch.zeros((1, 5), dtype=torch.float64, device=dev)
+        fin_ws = torch.empty(int(hb.lib().holo_ospr_finalize_workspace_size()), dtype=torch.uint8, device=dev)
 
     def ospr_stages(L, lut, T_in=None):
-        """(pre, C-1, post) of one OSPR step: a0 + this rank's shard, the all-reduce of the
-        partial intensity (sub-frame shards over N > 1 ranks), then mean + MSE (a7)."""
-        pre, coll, post = sharded.stages(T if T_in is None else T_in, S, lut[:L], ws, out, mse_buf,
-                                         phase_offset=frame_off)
+        """(pre, exchange) of one OSPR step: a0 + this rank's shard (the whole frame set, a7
+        fused, when it is not split); for a split, the exchange C-1 (reduce-scatter of the
+        partial intensity) + a7 on the owned rows + C-2 (five doubles) + MSE, eager (NCCL)."""
+        Tx = T if T_in is None else T_in
 
         def pre_a0():
             hb.lut_generate(LUT_SEED, L, out=lut[:L])                               # a0
-            pre()                                                                   # a1-a6 (shard)
-        return pre_a0, coll, post
+            if full:
+                out.mse = mse_buf
+                hb.ospr_generate(Tx, S, lut[:L], phase_offset=frame_off, workspace=ws, out=out)   # a1-a7
+            else:
+                hb.ospr_generate(Tx, S, lut[:L], phase_offset=frame_off, sf_range=(sb, se), want_mse=False,
+                                 workspace=ws, out=out)                             # a1-a6 (shard)
+
+        def exchange():
+            if not full:
+                sharded.exchange(Tx, out.intensity, S, mean_rows, sums_buf, mse_buf, None, fin_workspace=fin_ws)
+        exchange.local = full
+        return pre_a0, exchange
 
     def make_ospr_step(L, lut):
-        pre, coll, post = ospr_stages(L, lut)
+        pre, exch = ospr_stages(L, lut)
 
         def step():
             pre()
-            coll()                                                                  # C-1 (NCCL), N > 1
-            post()                                                                  # a7
+            exch()
         return step
 
     use_graph = not args.no_graph
@@ -359,7 +384,7 @@ def run_gpu(args):
     l0 = hb.launch_count()
     step()
     launches_per_step = hb.launch_count() - l0                 # libholo kernels in one step
-    timed_step = graphed_stages(*ospr_stages(args.lut, lut_buf), use_graph)
+    timed_step = graphed_stages(*ospr_stages(args.lut, lut_buf), None, use_graph)
     with Clocks(local) as clk:
         # the timed block lasts milliseconds; the sampler (100 ms period) sees the clocks of the
         # same step running untimed for 0.6 s right before it (extra warm-up, same load)
@@ -422,10 +447,12 @@ def run_gpu(args):
                    "n": n, "n_sub": S, "lut_len": args.lut, "lut_seed": LUT_SEED,
                    "l2": "flushed before every timed step (256 MiB write)",
                    "launch": ("CUDA graph replay of the step (captured once)" if sworld == 1 else
-                              "CUDA graph replays around the eager NCCL all-reduce") if use_graph else "eager launches",
+                              "CUDA graph replay of the shard, then the eager exchange (NCCL)") if use_graph
+                             else "eager launches",
                    "parallelism": (f"frame-set shards x{world}: rank r runs global frame set r (cursor off0 + "
                                    "r*N_SF*N^2), no collective" if frames_mode else
-                                   f"sub-frame shards x{sworld} + NCCL all-reduce of the intensity")},
+                                   f"sub-frame shards x{sworld} + NCCL reduce-scatter of the partial intensity "
+                                   "(C-1), a7 on the owned rows, NCCL all-reduce of 5 doubles (C-2)")},
         "gpu_launches": launches_timed,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
@@ -438,32 +465,6 @@ def run_gpu(args):
         "device": {"name": props.name, "sms": props.multi_processor_count,
                    "l2_mb": getattr(props, "L2_cache_size", 0) / 2 ** 20},
     }
-
-    # ---------------- N > 1: one frame set split over the ranks (C-1 over NCCL) ----------------
-    # HOLO_BENCH_FAKE_SHARDS=k (testing only, N = 1): run this block as rank 0 of k with a no-op
-    # collective, to exercise its code path on one GPU; its number is not a result
-    fake_sh = int(os.environ.get("HOLO_BENCH_FAKE_SHARDS", "0")) if world == 1 else 0
-    sh_world = fake_sh if fake_sh > 1 else world
-    if sh_world > 1 and frames_mode and sh_world <= S:   # every rank holds sub-frames (same collectives)
-        ssb, sse = shard_range(S, sh_world, rank)
-        sh = ShardedOspr(sh_world, rank, all_reduce=(lambda t: None)) if fake_sh > 1 else ShardedOspr(world, rank)
-        s_out = hb.OsprResult(bits=torch.empty((1, sse - ssb, n, n // 8), dtype=torch.uint8, device=dev),
-                              intensity=torch.empty((1, n, n), dtype=torch.float32, device=dev), mse=None)
-        s_mse = torch.empty(1, dtype=torch.float64, device=dev)
-        pre, coll, post = sh.stages(T, S, lut_buf[:args.lut], ws, s_out, s_mse)
-
-        def s_pre():
-            hb.lut_generate(LUT_SEED, args.lut, out=lut_buf[:args.lut])
-            pre()
-        sst = graphed_stages(s_pre, coll, post, use_graph)
-        stm, _ = timed_loop(sst, args.steps, args.warmup, world, flush)
-        stm = max_over_ranks(stm, world)
-        result["subframe_shards"] = {
-            "value": S * args.steps / (stm / 1e3), "unit": UNIT, "ms_per_step": stm / args.steps,
-            "scaling": "strong", "mse": float(s_mse.item()),
-            "what": f"one C3 frame set per step, its {S} sub-frames split over {sh_world} ranks "
-                    "(shard_range), NCCL all-reduce of the partial intensity, then mean + MSE on every rank "
-                    "(BASELINE configs[4]'s partition; graphs around the eager all-reduce)"}
 
     # ---------------- LUT sweep of C3 ----------------
     if not args.no_sweep and world == 1:
@@ -537,14 +538,13 @@ def run_gpu(args):
         T_dev = torch.empty_like(T)
         lut_e2e = hb.lut_generate(LUT_SEED, args.lut, device=dev)
 
-        pre, coll, post = ospr_stages(args.lut, lut_e2e, T_in=T_dev)
+        pre, coll = ospr_stages(args.lut, lut_e2e, T_in=T_dev)
 
         def e2e_pre():
             T_dev.copy_(T_host, non_blocking=True)                              # H2D inputs
             pre()                                                               # a0, a1-a6 (shard)
 
-        def e2e_post():
-            post()                                                              # a7
+        def e2e_post():                                                         # (a7 in the exchange)
             mse_host.copy_(mse_buf, non_blocking=True)                          # D2H metric
             bits_host.copy_(out.bits, non_blocking=True)                        # D2H holograms
         tm, _ = timed_loop(graphed_stages(e2e_pre, coll, e2e_post, use_graph), args.steps, args.warmup, world,
@@ -558,7 +558,7 @@ def run_gpu(args):
                                                                 if use_graph else "eager")}
 
     # ---------------- OSPR C5 frame sets (2048^2, N_SF = 32) ----------------
-    if not args.no_c5 and frames_mode:
+    if not args.no_c5 and world == 1:
         w5 = WORKLOADS["C5"]
         n5, S5, P5 = w5.n, w5.n_sub, w5.n * w5.n
         T5 = torch.from_numpy(target_for(w5, rank)).to(dev)     # rank r: frame r of the video
@@ -588,6 +588,10 @@ def run_gpu(args):
                        "launch": "CUDA graph replay" if use_graph else "eager launches"},
         }
         del ws5
+
+    # ---------------- OSPR C5 video: sub-frame shards + C-1/C-2 on a side stream (configs[4]) ----------------
+    if not args.no_c5:
+        result["c5_video"] = c5_video(args, hb, world, rank, dev, flush)
 
     # ---------------- GS C4 ----------------
     if not args.no_gs:
@@ -642,6 +646,97 @@ def run_gpu(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result))
+
+
+def c5_video(args, hb, world, rank, dev, flush):
+    """BASELINE configs[4]: a stream of 2048^2 video frames, N_SF = 32 binary sub-frames each,
+    the sub-frames of every frame sharded over the ranks (SubframeShardPipeline): per frame a0 +
+    this rank's shard on the compute stream; C-1 reduce-scatter of the partial intensity (each
+    rank owns 2048/N rows), a7 on the owned rows, C-2 all-reduce of five doubles and the MSE on
+    a side stream, overlapping the next frame's passes.  Timed from the first frame's launch to
+    the last frame's MSE (CUDA events, max over ranks).  At N = 1 the same stream runs whole
+    frames with the fused a7 and no collective.  HOLO_BENCH_FAKE_SHARDS=k (N = 1, testing only):
+    rank 0 of a k-way split with stand-in collectives (own slice, no exchange) -- not a result."""
+    import torch
+    from holo_synth import LUT_SEED, WORKLOADS, target_for
+    from paper_2004_04049_b200.parallel import SubframeShardPipeline
+    w5 = WORKLOADS["C5"]
+    n5, S5, P5, L5 = w5.n, w5.n_sub, w5.n * w5.n, w5.lut_lens[0]
+    fake = int(os.environ.get("HOLO_BENCH_FAKE_SHARDS", "0")) if world == 1 else 0
+    sworld = fake if fake > 1 else world
+    nt = 4                                                     # distinct seeded targets, cycled
+    Ts = [torch.from_numpy(target_for(w5, f)).to(dev) for f in range(nt)]
+    lut5 = torch.empty(L5, dtype=torch.complex64, device=dev)
+    kw = {}
+    if fake > 1:
+        kw = dict(reduce_scatter=lambda o, i: o.copy_(i[:o.numel()]), all_reduce=lambda t: None)
+    pipe = SubframeShardPipeline(n5, S5, sworld, rank, lut5, depth=2,
+                                 before_each=lambda: hb.lut_generate(LUT_SEED, L5, out=lut5), **kw)
+    kf = max(16, args.steps)                                   # frames streamed per timed run
+    for f in range(max(args.warmup, 3)):
+        pipe.submit(Ts[f % nt])
+    pipe.drain()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    reps = []
+    for _ in range(3):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.compute)
+        for f in range(kf):
+            pipe.submit(Ts[f % nt])
+        (pipe.side if sworld > 1 else pipe.compute).wait_stream(pipe.compute)
+        b.record(pipe.side if sworld > 1 else pipe.compute)
+        torch.cuda.synchronize()
+        barrier(world)
+        reps.append(max_over_ranks(a.elapsed_time(b), world))
+    tm = statistics.median(reps)
+    mse_last = float(pipe.result(pipe.f - 1)[2].item())
+    # the parts alone: one frame's compute (a0 + shard) and, N > 1, one C-1 reduce-scatter
+    sb, se = pipe.sf
+    comp = []
+    for _ in range(3):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.compute)
+        pipe.submit(Ts[0])
+        b.record(pipe.compute)
+        torch.cuda.synchronize()
+        comp.append(a.elapsed_time(b))
+    c1 = None
+    if world > 1:
+        import torch.distributed as dist
+        inp = torch.ones(n5 * n5, dtype=torch.float32, device=dev)
+        outp = torch.empty(n5 * n5 // world, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            dist.reduce_scatter_tensor(outp, inp)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            dist.reduce_scatter_tensor(outp, inp)
+        b.record()
+        torch.cuda.synchronize()
+        c1 = max_over_ranks(a.elapsed_time(b) / 10, world)
+    return {
+        "metric": "OSPR 2048^2 binary sub-frames/s (video stream, sub-frame shards)", "unit": UNIT,
+        "value": S5 * kf / (tm / 1e3), "ms_per_frame": tm / kf, "frames_timed": kf, "runs_ms": reps,
+        "statistic": "median of 3 runs", "scaling": "strong" if sworld > 1 else "n/a (one GPU)",
+        "mse_last_frame": mse_last,
+        "shard": {"sub_frames": [sb, se], "owned_rows": list(pipe.rows) if sworld > 1 else [0, n5]},
+        "compute_ms_per_frame": statistics.median(comp),
+        "c1_reduce_scatter_ms": c1,
+        "c1_bytes": 4 * P5 if sworld > 1 else 0,
+        "config": {"workload": "C5: OSPR 2048x2048 binary video, N_SF=32, LUT 2^16 (a0 per frame), frames "
+                               f"streamed back to back ({nt} seeded targets cycled); BASELINE configs[4]",
+                   "partition": (f"sub-frame shards x{sworld} (whole pairs, subframe_range), C-1 NCCL reduce-scatter of the "
+                                 "partial intensity (fp32, N^2/world per rank), a7 on the owned rows, C-2 NCCL "
+                                 "all-reduce of 5 doubles, MSE -- on a side stream overlapping the next frame"
+                                 if sworld > 1 else "whole frames on one GPU, fused a7, no collective") +
+                                (" [FAKE: stand-in collectives, not a result]" if fake > 1 else ""),
+                   "l2": "flushed once before each timed run of kf frames", "launch": "eager launches, two streams"},
+    }
 
 
 # ---------------------------------------------------------------------------------------------

@@ -175,6 +175,29 @@ holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, 
                                float *intensity_mean, double *mse, void *ws, size_t ws_bytes,
                                holo_stream stream);
 
+/* Step a7 on one frame's row slice, for sub-frame shards finished by a
+ * reduce-scatter (each rank owns rows [row0, row1) of the
+ * summed intensity) and a 5-double all-reduce (C-2):
+ *   intensity_mean_rows = intensity_sum_rows / n_sub   (in place allowed)
+ *   sums[5] = (sum I, sum I^2, sum I T^2, sum T^2, sum T^4) over omega
+ *             restricted to the slice, fp64, fixed reduction order
+ * The MSE is nonlinear in I (P:64 averages intensities, R-12 normalises the
+ * average), so ranks add their `sums` (C-2) and only then evaluate
+ * holo_ospr_mse_from_sums.  target [n][n] (the whole frame);
+ * intensity_sum_rows, intensity_mean_rows [row1-row0][n]; sums: 5 doubles of
+ * device memory; ws: holo_ospr_finalize_workspace_size() bytes.
+ * INVALID_ARG for an empty or out-of-range slice; WORKSPACE if ws is short. */
+holo_status holo_ospr_finalize_rows(const float *target, const float *intensity_sum_rows, int32_t n,
+                                    int32_t row0, int32_t row1, int32_t n_sub, holo_region omega,
+                                    float *intensity_mean_rows, double *sums, void *ws, size_t ws_bytes,
+                                    holo_stream stream);
+
+/* R-12 from reduced sums: mse[f] = (a^2 S_II - 2 a S_IT2 + S_T4) / |omega| with
+ * a = S_T2 / S_I (0 if S_I = 0), for sums [n_frames][5] as written by
+ * holo_ospr_finalize_rows and summed over the ranks (device pointers). */
+holo_status holo_ospr_mse_from_sums(const double *sums, int32_t n_frames, holo_region omega, double *mse,
+                                    holo_stream stream);
+
 /* ------------------------------------------------------------------------
  * GS -- Gerchberg-Saxton (Fig. 2 left), frames independent.
  * For frame b in [0, batch):

@@ -19,7 +19,8 @@ import torch
 from ._lib import HoloRegion, check, lib
 
 __all__ = [
-    "lut_generate", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize", "gs_workspace_bytes",
+    "lut_generate", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize",
+    "ospr_finalize_rows", "ospr_mse_from_sums", "gs_workspace_bytes",
     "gs_generate", "gs_step", "fft2", "debug_randomise", "debug_ospr_pairs", "launch_count", "profile_enable", "profile_read",
     "kernel_names", "version", "default_omega", "OsprResult", "GsResult",
 ]
@@ -181,6 +182,48 @@ def ospr_finalize(target: torch.Tensor, intensity_sum: torch.Tensor, n_sub: int,
     check(lib().holo_ospr_finalize(t3.data_ptr(), intensity_sum.data_ptr(), n, F, n_sub, _region(om),
                                    out.data_ptr(), _ptr(mse), ws.data_ptr(), ws.numel(), _stream(t3.device)))
     return out, mse
+
+
+def ospr_finalize_rows(target: torch.Tensor, intensity_sum_rows: torch.Tensor, row0: int, n_sub: int,
+                       omega: Optional[Sequence[int]] = None, out: Optional[torch.Tensor] = None,
+                       sums_out: Optional[torch.Tensor] = None,
+                       workspace: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Step a7 on rows [row0, row0 + rows) of one frame (the slice a rank owns after the
+    reduce-scatter C-1): the mean (in place if out is intensity_sum_rows) and the five fp64
+    partial sums of R-12 over omega within the slice, to be all-reduced (C-2) before
+    ospr_mse_from_sums.  target: the whole frame [N][N]; intensity_sum_rows: [rows][N]."""
+    _need(target, torch.float32, "target")
+    _need(intensity_sum_rows, torch.float32, "intensity_sum_rows")
+    n = target.shape[-1]
+    t2 = target.reshape(n, n) if target.numel() == n * n else None
+    if t2 is None:
+        raise ValueError("target must be one [N][N] frame")
+    rows = intensity_sum_rows.numel() // n
+    if intensity_sum_rows.numel() != rows * n or rows < 1:
+        raise ValueError("intensity_sum_rows must hold whole rows of N")
+    om = omega if omega is not None else default_omega(n, "ospr")
+    dev = target.device
+    out = torch.empty_like(intensity_sum_rows) if out is None else \
+        _need_out(out, torch.float32, tuple(intensity_sum_rows.shape), dev, "out")
+    sums = torch.empty(5, dtype=torch.float64, device=dev) if sums_out is None else \
+        _need_out(sums_out, torch.float64, (5,), dev, "sums_out")
+    ws = _workspace(workspace, int(lib().holo_ospr_finalize_workspace_size()), dev)
+    check(lib().holo_ospr_finalize_rows(t2.data_ptr(), intensity_sum_rows.data_ptr(), n, row0, row0 + rows, n_sub,
+                                        _region(om), out.data_ptr(), sums.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        _stream(dev)))
+    return out, sums
+
+
+def ospr_mse_from_sums(sums: torch.Tensor, omega: Sequence[int], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """R-12 from reduced sums [F][5] (float64, device) -> mse [F]."""
+    _need(sums, torch.float64, "sums")
+    F = sums.numel() // 5
+    if sums.numel() != 5 * F or F < 1:
+        raise ValueError("sums must be [F][5]")
+    out = torch.empty(F, dtype=torch.float64, device=sums.device) if out is None else \
+        _need_out(out, torch.float64, (F,), sums.device, "out")
+    check(lib().holo_ospr_mse_from_sums(sums.data_ptr(), F, _region(omega), out.data_ptr(), _stream(sums.device)))
+    return out
 
 
 # ---- GS ------------------------------------------------------------------------------------------

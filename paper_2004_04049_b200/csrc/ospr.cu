@@ -930,6 +930,69 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
     }
 }
 
+// ---- a7 on a row slice (the owned slice after a cross-rank reduce-scatter, C-1) ---------------
+// Rows [row0, row0 + nrows) of one frame: mean = sum * scale (in place allowed) and the five
+// fp64 partial sums (sum I, I^2, I T^2, T^2, T^4) over Omega restricted to the slice, one slot
+// per CTA; the last CTA (ticket) reduces the slots in CTA order (deterministic) into sums[5].
+// kFinThreads threads, `iter` pixels per thread, grid fixed by (n, nrows).
+__global__ void __launch_bounds__(kFinThreads)
+ospr_finalize_rows_kernel(const float *__restrict__ acc, const float *__restrict__ T, int n, int row0, int nrows,
+                          int iter, float scale, float *__restrict__ out, holo_region om,
+                          double *__restrict__ parts, unsigned *counter, double *__restrict__ sums)
+{
+    HOLO_PDL_ENTRY();
+    const int pix = n * nrows;
+    double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < iter; ++i) {
+        const int k = (int)blockIdx.x * kFinThreads + (int)threadIdx.x + i * (int)gridDim.x * kFinThreads;
+        if (k >= pix)
+            break;
+        const int y = row0 + k / n, x = k % n;
+        const float I = __ldg(acc + k) * scale;
+        out[k] = I;
+        if (y >= om.row0 && y < om.row1 && x >= om.col0 && x < om.col1) {
+            const double Id = I, tt = __ldg(T + (size_t)y * n + x), t2 = tt * tt;
+            s[0] += Id;
+            s[1] += Id * Id;
+            s[2] += Id * t2;
+            s[3] += t2;
+            s[4] += t2 * t2;
+        }
+    }
+    block_reduce_store(s, 5, parts + (size_t)blockIdx.x * 5);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        __threadfence();                                   // this CTA's slot before its ticket
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last)
+        return;
+    __threadfence();
+    double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+        for (int i = 0; i < 5; ++i)
+            t[i] += __ldcg(parts + (size_t)b * 5 + i);
+    __shared__ double o[5];
+    __syncthreads();
+    block_reduce_store(t, 5, o);
+    __syncthreads();
+    if (threadIdx.x < 5)
+        sums[threadIdx.x] = o[threadIdx.x];
+    if (threadIdx.x == 0)
+        *counter = 0u;
+}
+
+// R-12 from the five (cross-rank reduced) sums of each frame (C-2 done by the caller).
+__global__ void ospr_mse_from_sums_kernel(const double *__restrict__ sums, int n_frames, double inv_count,
+                                          double *__restrict__ mse)
+{
+    HOLO_PDL_ENTRY();
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < n_frames)
+        mse[f] = mse_from_sums(sums + (size_t)f * 5, inv_count);
+}
+
 // ---- host orchestration -------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -1247,6 +1310,48 @@ extern "C" holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int
         return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }
 #undef HOLO_PAIRS_CASE
+}
+
+extern "C" holo_status holo_ospr_finalize_rows(const float *target, const float *intensity_sum_rows, int32_t n,
+                                               int32_t row0, int32_t row1, int32_t n_sub, holo_region omega,
+                                               float *intensity_mean_rows, double *sums, void *ws, size_t ws_bytes,
+                                               holo_stream stream)
+{
+    HOLO_TRY(check_n(n));
+    HOLO_CHECK_ARG(0 <= row0 && row0 < row1 && row1 <= n, "row slice [%d,%d) must be a non-empty part of [0,%d)",
+                   row0, row1, n);
+    HOLO_CHECK_ARG(n_sub >= 1, "n_sub must be >= 1");
+    HOLO_CHECK_ARG(target && intensity_sum_rows && intensity_mean_rows && sums,
+                   "target, intensity_sum_rows, intensity_mean_rows and sums are required");
+    HOLO_TRY(check_region(omega, n));
+    HOLO_CHECK_ARG(ws != nullptr, "workspace is NULL");
+    if (ws_bytes < kFinWsBytes)
+        return set_error(HOLO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, kFinWsBytes);
+    const int nrows = row1 - row0, pix = n * nrows;
+    int fb = (pix + 8 * kFinThreads - 1) / (8 * kFinThreads);
+    if (fb > kFinBlocks)
+        fb = kFinBlocks;
+    const int iter = (pix + fb * kFinThreads - 1) / (fb * kFinThreads);
+    double *parts = (double *)ws;
+    unsigned *counter = finalize_ticket(parts);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess)
+        return cuda_status(e, "cudaMemsetAsync(finalize ticket)");
+    return launch(K_OSPR_FINALIZE, ospr_finalize_rows_kernel, dim3(fb), dim3(kFinThreads), 0, s,
+                  intensity_sum_rows, target, n, row0, nrows, iter, 1.0f / (float)n_sub, intensity_mean_rows, omega, parts,
+                  counter, sums);
+}
+
+extern "C" holo_status holo_ospr_mse_from_sums(const double *sums, int32_t n_frames, holo_region omega, double *mse,
+                                               holo_stream stream)
+{
+    HOLO_CHECK_ARG(sums != nullptr && mse != nullptr, "sums and mse are required");
+    HOLO_CHECK_ARG(n_frames >= 1, "n_frames must be >= 1");
+    HOLO_CHECK_ARG(omega.row0 < omega.row1 && omega.col0 < omega.col1, "omega is empty");
+    const double cnt = (double)(omega.row1 - omega.row0) * (double)(omega.col1 - omega.col0);
+    return launch(K_MSE_REDUCE, ospr_mse_from_sums_kernel, dim3((n_frames + 127) / 128), dim3(128), 0,
+                  (cudaStream_t)stream, sums, n_frames, 1.0 / cnt, mse);
 }
 
 extern "C" holo_status holo_ospr_finalize(const float *target, const float *intensity_sum, int32_t n,
