@@ -456,6 +456,7 @@ def run_gpu(args):
         "gpu_launches": launches_timed,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "dram_frac": (traffic / (kern[dom]["avg_us"] * 1e-6) / 1e9 / hbm_peak) if traffic else None,
                      "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": kern[dom]["avg_us"],
                      "share_of_step": share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                      "peak_spec": HBM_SPEC_GBS, "frac_spec": achieved / HBM_SPEC_GBS},
@@ -624,6 +625,7 @@ def run_gpu(args):
         gbytes = {"gs_cols": 16 * P4 * g, "gs_rows": 20 * P4 * g}
         gdom = max(gbytes, key=lambda k: gk.get(k, {"total_ms": 0})["total_ms"])
         gach = gbytes[gdom] / (gk[gdom]["avg_us"] * 1e-6) / 1e9
+        gtraffic, gtraffic_src = ncu_traffic(gdom)   # DRAM bytes per launch at C4 size (64 frames)
         result["gs"] = {
             "metric": "GS 1024^2 iterations/s", "unit": "frame-iterations/s",
             "value": B * iters * ks / (gm / 1e3), "ms_per_step": gm / ks, "steps": ks,
@@ -633,7 +635,10 @@ def run_gpu(args):
             "roofline": {"bound": "hbm", "kernel": gdom, "achieved": gach, "peak": hbm_peak, "unit": "GB/s",
                          "frac": gach / hbm_peak, "algorithmic_bytes_per_launch": gbytes[gdom],
                          "avg_launch_us": gk[gdom]["avg_us"], "peak_spec": HBM_SPEC_GBS,
-                         "frac_spec": gach / HBM_SPEC_GBS},
+                         "frac_spec": gach / HBM_SPEC_GBS,
+                         "traffic": gtraffic, "traffic_source": gtraffic_src,
+                         "dram_frac": (gtraffic / (gk[gdom]["avg_us"] * 1e-6) / 1e9 / hbm_peak
+                                       if gtraffic else None)},
             "fft": fft_rate(B * iters * ks / (gm / 1e3), P4, paired=False),
             "kernels": gk,
         }

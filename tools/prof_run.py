@@ -1,4 +1,5 @@
-"""Small driver for ncu captures: runs the C3 OSPR step and a short C4-shaped GS
+"""Small driver for ncu captures: runs the C3 OSPR step and a short C4-shaped GS (gs: 8 frames;
+gs64: all 64 frames of C4 in one launch group, its 512 MiB state streaming from HBM)
 (profile with -k regex:<kernel> -s <skip> -c <count>)."""
 import os
 import sys
@@ -21,9 +22,10 @@ if what in ("all", "ospr"):
         r = hb.ospr_generate(T, w.n_sub, lut)
     torch.cuda.synchronize()
     print("ospr mse", r.mse.item())
-if what in ("all", "gs"):
+if what in ("all", "gs", "gs64"):
     w = WORKLOADS["C4"]
-    T = torch.from_numpy(np.stack([target_for(w, b) for b in range(8)])).to(dev)
+    nfr = w.frames if what == "gs64" else 8          # gs64: the whole C4 launch group (512 MiB state)
+    T = torch.from_numpy(np.stack([target_for(w, b) for b in range(nfr)])).to(dev)
     lut = hb.lut_generate(LUT_SEED, 1 << 16)
     for _ in range(reps):
         g = hb.gs_generate(T, 3, lut, levels=0)
