@@ -57,6 +57,7 @@ def lib():
                 "or_lut_index": (_u64, [_u64, _u64]),
                 "or_apply_phase": (None, [_F, _i, _F, _u64, _u64, _D]),
                 "or_apply_phase_prng": (None, [_F, _i, _u64, _u64, _D]),
+                "or_apply_phase_prng_q": (None, [_F, _i, _u64, _u64, _i, _D]),
                 "or_dft2_direct": (None, [_D, _D, _i, _i, _i]),
                 "or_dft2_separable": (None, [_D, _D, _i, _i, _i]),
                 "or_fft2": (_i, [_D, _i, _i]),
@@ -145,6 +146,16 @@ def apply_phase_prng(T, seed: int, cursor: int) -> np.ndarray:
     n = T.shape[0]
     R = np.empty((n, n), dtype=np.complex128)
     lib().or_apply_phase_prng(_p(T, _F), n, seed, cursor, _p(R, _D))
+    return R
+
+
+def apply_phase_prng_q(T, seed: int, cursor: int, q: int) -> np.ndarray:
+    """P:170 / R-25: the PRNG source with phases quantised to 2^q levels (a 2^q-entry
+    sin/cos table): R = T * R5(u_g truncated to its top q bits)."""
+    T = _f32(T)
+    n = T.shape[0]
+    R = np.empty((n, n), dtype=np.complex128)
+    lib().or_apply_phase_prng_q(_p(T, _F), n, seed, cursor, q, _p(R, _D))
     return R
 
 

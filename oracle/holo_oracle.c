@@ -182,6 +182,23 @@ void or_apply_phase_prng(const float *T, int n, uint64_t seed, uint64_t cursor, 
     }
 }
 
+/* The paper's runtime-flexible alternative ("PRNGs with LUTs for sin
+ * and cosine functions"; R-25): a PRNG per draw, its phase quantised to
+ * 2^q levels so that (cos, sin) comes from a 2^q-entry table.  Draw g takes
+ * the top q bits of the angle code, i.e. the code truncated to a multiple of
+ * 2^(32-q), and the recipe at that code -- written out here without a table:
+ * phase(g) = R-5(u_g & ~(2^(32-q) - 1)), 1 <= q <= 32 (q = 32: or_apply_phase_prng). */
+void or_apply_phase_prng_q(const float *T, int n, uint64_t seed, uint64_t cursor, int q, cplx *R)
+{
+    uint64_t P = (uint64_t)n * (uint64_t)n;
+    uint32_t mask = q >= 32 ? 0xFFFFFFFFu : ~((1u << (32 - q)) - 1u);
+    for (uint64_t p = 0; p < P; ++p) {
+        float c, s;
+        or_phase_f32(or_angle_code(seed, cursor + p) & mask, &c, &s);
+        R[p] = (double)T[p] * ((double)c + I * (double)s);
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* A1-A3: the unitary DFT pair (Eqs. (1)-(2)) and its FFT */
 /* ------------------------------------------------------------------ */

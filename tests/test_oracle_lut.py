@@ -145,3 +145,52 @@ def test_full_length_lut_equals_prng_stream():
     for s in range(3):
         assert np.array_equal(oracle.apply_phase(T, lut, s * n * n),
                               oracle.apply_phase_prng(T, 2004, s * n * n))
+
+
+# ---- P:170 / R-25: PRNG + a 2^q-entry sin/cos table ----------------------------------------------
+
+def _codes(seed, cursor, m):
+    return np.array([oracle.angle_code(seed, cursor + k) for k in range(m)], dtype=np.uint64)
+
+
+def test_prng_table_q2_is_quarter_turns_exactly():
+    """q = 2: the phase is i^(u >> 30) exactly (cos, sin in {0, +-1}), so R = T * i^k with no
+    rounding at all -- a closed form that a wrong shift, mask or octant would break."""
+    n, seed, cur = 16, 2004, 12345
+    T = np.linspace(0.1, 1.0, n * n, dtype=np.float32).reshape(n, n)
+    R = oracle.apply_phase_prng_q(T, seed, cur, 2)
+    k = (_codes(seed, cur, n * n) >> 30).astype(np.int64).reshape(n, n)
+    assert np.array_equal(R, T.astype(np.float64) * (1j ** k))
+
+
+def test_prng_table_q3_eighth_turns_and_q32_is_the_prng_source():
+    n, seed, cur = 16, 7, 99
+    T = np.ones((n, n), np.float32)
+    R = oracle.apply_phase_prng_q(T, seed, cur, 3)
+    k = (_codes(seed, cur, n * n) >> 29).astype(np.float64).reshape(n, n)
+    assert np.max(np.abs(R - np.exp(2j * np.pi * k / 8))) <= 2.0 ** -24
+    # no truncation: the full-precision on-the-fly source
+    assert np.array_equal(oracle.apply_phase_prng_q(T, seed, cur, 32), oracle.apply_phase_prng(T, seed, cur))
+
+
+@pytest.mark.parametrize("q", [5, 8, 12, 16])
+def test_prng_table_levels(q):
+    """The phase of draw g is the angle of the top q bits of its code, 2 pi (u >> (32-q)) / 2^q,
+    at unit modulus (fp32 rounding of the recipe: 1e-7)."""
+    n, seed, cur = 32, 11, 5
+    T = np.ones((n, n), np.float32)
+    R = oracle.apply_phase_prng_q(T, seed, cur, q)
+    k = (_codes(seed, cur, n * n) >> (32 - q)).astype(np.float64).reshape(n, n)
+    assert np.max(np.abs(R - np.exp(2j * np.pi * k / 2 ** q))) <= 1e-7
+    assert np.max(np.abs(np.abs(R) - 1)) <= 1e-7
+
+
+def test_prng_table_levels_uniform_chi2():
+    """S:179's uniformity check on the quantised source: the 256 levels of q = 8 over 2^16
+    draws pass a chi^2 test at p = 0.001 (critical value of chi^2 with 255 dof: 330.5)."""
+    n, seed = 256, 2004
+    R = oracle.apply_phase_prng_q(np.ones((n, n), np.float32), seed, 0, 8)
+    lev = np.rint(np.mod(np.angle(R), 2 * np.pi) * 256 / (2 * np.pi)).astype(np.int64) % 256
+    cnt = np.bincount(lev.ravel(), minlength=256)
+    exp = n * n / 256
+    assert ((cnt - exp) ** 2 / exp).sum() < 330.5
