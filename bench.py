@@ -488,6 +488,20 @@ def run_gpu(args):
         sweep["prng"] = {"sub_frames_per_s": S * ks / (tm / 1e3), "ms_per_step": tm / ks,
                          "mse": float(out.mse.item()),
                          "what": "phases drawn on the fly (holo_ospr_generate_prng), no LUT"}
+        # P:170's runtime-flexible alternative (R-25): SplitMix64 per draw indexing a 2^q sin/cos table
+        for q in (8, 12, 16):
+            tbl = torch.empty(1 << q, dtype=torch.complex64, device=dev)
+
+            def table_step(q=q, tbl=tbl):
+                hb.phase_table(q, out=tbl)
+                hb.ospr_generate(T, S, prng_seed=LUT_SEED, phase_bits=q, table=tbl, workspace=ws, out=out)
+            st = graphed(table_step, use_graph)
+            tm, _ = timed_loop(st, ks, 2, world, flush)
+            sweep[f"prng_table_q{q}"] = {"sub_frames_per_s": S * ks / (tm / 1e3), "ms_per_step": tm / ks,
+                                         "mse": float(out.mse.item()),
+                                         "what": f"SplitMix64 per draw + a 2^{q}-entry sin/cos table "
+                                                 "(holo_ospr_generate_prng_table; phases quantised to "
+                                                 f"{1 << q} levels)"}
         result["lut_sweep"] = sweep
         del big
 

@@ -161,6 +161,26 @@ holo_status holo_ospr_generate_prng(const float *target, int32_t n, int32_t n_fr
                                     int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse,
                                     holo_region omega, void *ws, size_t ws_bytes, holo_stream stream);
 
+/* The paper's runtime-flexible alternative ("PRNGs with LUTs for sin
+ * and cosine functions are expected to remain the dominant technique";
+ * reading R-25): the draws of holo_ospr_generate_prng, their phases quantised
+ * to 2^phase_bits levels so that (cos, sin) comes from a small table instead
+ * of the recipe: draw g uses table[u_g >> (32 - phase_bits)], u_g the high
+ * word of SplitMix64(seed, g).
+ *   holo_phase_table   table[k] = R-5 at the angle code k << (32 - phase_bits),
+ *                      i.e. (cos, sin)(2 pi k / 2^phase_bits), k < 2^phase_bits;
+ *                      table: device, 2^phase_bits holo_c64, 16-byte aligned
+ *   holo_ospr_generate_prng_table  as holo_ospr_generate_prng, with `table`
+ *                      (from holo_phase_table with the same phase_bits; read
+ *                      only) replacing the per-draw recipe
+ * phase_bits in [1, 16], else INVALID_ARG. */
+holo_status holo_phase_table(int32_t phase_bits, holo_c64 *table, holo_stream stream);
+holo_status holo_ospr_generate_prng_table(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
+                                          uint64_t seed, const holo_c64 *table, int32_t phase_bits,
+                                          uint64_t phase_offset, int32_t sf_begin, int32_t sf_end,
+                                          uint8_t *holo_bits, float *intensity, double *mse,
+                                          holo_region omega, void *ws, size_t ws_bytes, holo_stream stream);
+
 /* Mean intensity and MSE from a summed intensity (after the caller's
  * cross-rank sum of holo_ospr_generate partial sums): intensity_mean =
  * intensity_sum / n_sub (in place allowed), mse as step a7.

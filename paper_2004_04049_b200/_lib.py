@@ -48,6 +48,9 @@ SIGNATURES = {
                                      HoloRegion, _vp, _sz, _vp]),
     "holo_ospr_generate_prng": (C.c_int, [_vp, _i32, _i32, _i32, _u64, _u64, _i32, _i32, _vp, _vp, _vp,
                                           HoloRegion, _vp, _sz, _vp]),
+    "holo_phase_table": (C.c_int, [_i32, _vp, _vp]),
+    "holo_ospr_generate_prng_table": (C.c_int, [_vp, _i32, _i32, _i32, _u64, _vp, _i32, _u64, _i32, _i32, _vp, _vp,
+                                                _vp, HoloRegion, _vp, _sz, _vp]),
     "holo_ospr_finalize": (C.c_int, [_vp, _vp, _i32, _i32, _i32, HoloRegion, _vp, _vp, _vp, _sz, _vp]),
     "holo_ospr_finalize_rows": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, HoloRegion, _vp, _vp, _vp, _sz, _vp]),
     "holo_ospr_mse_from_sums": (C.c_int, [_vp, _i32, HoloRegion, _vp, _vp]),

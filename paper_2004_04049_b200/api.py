@@ -19,7 +19,7 @@ import torch
 from ._lib import HoloRegion, check, lib
 
 __all__ = [
-    "lut_generate", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize",
+    "lut_generate", "phase_table", "ospr_workspace_bytes", "ospr_chunk_pairs", "gs_group_frames", "ospr_generate", "ospr_finalize",
     "ospr_finalize_rows", "ospr_mse_from_sums", "gs_workspace_bytes",
     "gs_generate", "gs_step", "fft2", "debug_randomise", "debug_ospr_pairs", "launch_count", "profile_enable", "profile_read",
     "kernel_names", "version", "default_omega", "OsprResult", "GsResult",
@@ -101,6 +101,18 @@ def lut_generate(seed: int, n_lut: int, device=None, out: Optional[torch.Tensor]
     return out
 
 
+def phase_table(phase_bits: int, device=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The sin/cos table of the quantised PRNG source (R-25): complex64 [2^phase_bits],
+    entry k = (cos, sin)(2 pi k / 2^phase_bits) by recipe R-5."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    m = 1 << phase_bits
+    if out is None:
+        out = torch.empty(m, dtype=torch.complex64, device=dev)
+    _need_out(out, torch.complex64, (m,), out.device, "out")
+    check(lib().holo_phase_table(phase_bits, out.data_ptr(), _stream(out.device)))
+    return out
+
+
 # ---- OSPR --------------------------------------------------------------------------------------
 
 @dataclass
@@ -127,9 +139,12 @@ def gs_group_frames(n: int, batch: int) -> int:
 def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] = None, phase_offset: int = 0,
                   sf_range: Optional[Tuple[int, int]] = None, want_bits: bool = True, want_mse: bool = True,
                   omega: Optional[Sequence[int]] = None, workspace: Optional[torch.Tensor] = None,
-                  out: Optional[OsprResult] = None, prng_seed: Optional[int] = None) -> OsprResult:
+                  out: Optional[OsprResult] = None, prng_seed: Optional[int] = None,
+                  phase_bits: Optional[int] = None, table: Optional[torch.Tensor] = None) -> OsprResult:
     """OSPR over target [F][N][N] (or [N][N]); see holo_ospr_generate.  With prng_seed the
-    phases are drawn on the fly (holo_ospr_generate_prng) and `lut` must be None."""
+    phases are drawn on the fly (holo_ospr_generate_prng) and `lut` must be None; with
+    prng_seed and phase_bits = q the draws index a 2^q sin/cos table instead of running the
+    recipe (holo_ospr_generate_prng_table; `table` from phase_table(q), built if None)."""
     _need(target, torch.float32, "target")
     t3 = target if target.dim() == 3 else target.unsqueeze(0)
     F, n, _ = t3.shape
@@ -149,6 +164,16 @@ def ospr_generate(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor] 
         _need_out(out.intensity, torch.float32, (F, n, n), dev, "out.intensity")
         _need_out(out.mse, torch.float64, (F,), dev, "out.mse")
     workspace = _workspace(workspace, ospr_workspace_bytes(n, F, n_sub), dev)
+    if prng_seed is not None and phase_bits is not None:
+        if lut is not None:
+            raise ValueError("pass either lut or prng_seed, not both")
+        tbl = table if table is not None else phase_table(phase_bits, device=dev)
+        _need_out(tbl, torch.complex64, (1 << phase_bits,), dev, "table")
+        check(lib().holo_ospr_generate_prng_table(t3.data_ptr(), n, F, n_sub, prng_seed & 0xFFFFFFFFFFFFFFFF,
+                                                  tbl.data_ptr(), phase_bits, phase_offset, b, e, _ptr(out.bits),
+                                                  out.intensity.data_ptr(), _ptr(out.mse), _region(om),
+                                                  workspace.data_ptr(), workspace.numel(), _stream(dev)))
+        return out
     if prng_seed is not None:
         if lut is not None:
             raise ValueError("pass either lut or prng_seed, not both")
@@ -320,16 +345,21 @@ def debug_randomise(target: torch.Tensor, lut: Optional[torch.Tensor], offset: i
 # ---- instrumentation -------------------------------------------------------------------------------------
 
 def debug_ospr_pairs(target: torch.Tensor, n_sub: int, lut: Optional[torch.Tensor], offset: int = 0,
-                     sf_range: Optional[Tuple[int, int]] = None, prng_seed: Optional[int] = None) -> torch.Tensor:
+                     sf_range: Optional[Tuple[int, int]] = None, prng_seed: Optional[int] = None,
+                     phase_bits: Optional[int] = None) -> torch.Tensor:
     """Test hook: pass A's randomisation (conj of the Hermitian-paired Z) for frame 0's
-    sub-frame pairs in sf_range; complex64 [pairs][N][N]."""
+    sub-frame pairs in sf_range; complex64 [pairs][N][N].  prng_seed: the on-the-fly source;
+    with phase_bits = q also the 2^q sin/cos table source."""
     _need(target, torch.float32, "target")
     n = target.shape[-1]
     b, e = sf_range if sf_range is not None else (0, n_sub)
     out = torch.empty(((e - b + 1) // 2, n, n), dtype=torch.complex64, device=target.device)
     lp, L = _lut_args(lut)
-    use_prng = prng_seed is not None
-    check(lib().holo_debug_ospr_pairs(target.data_ptr(), n, n_sub, lp, L, int(use_prng), prng_seed or 0, offset, b, e,
+    use_prng = 0 if prng_seed is None else (1 if phase_bits is None else 2)
+    if use_prng == 2:
+        tbl = phase_table(phase_bits, device=target.device)
+        lp, L = tbl.data_ptr(), phase_bits
+    check(lib().holo_debug_ospr_pairs(target.data_ptr(), n, n_sub, lp, L, use_prng, prng_seed or 0, offset, b, e,
                                       out.data_ptr(),
                                       _stream(target.device)))
     return out

@@ -182,7 +182,8 @@ __device__ __forceinline__ float rsqrt_rn(float x) { return __frsqrt_rn(x); }
 // hardware divide: L >= N needs at most one subtraction; a power-of-two L is a mask;
 // otherwise Lemire's fastmod (exact for 32-bit operands).  An empty pool (N_LUT = 0,
 // R-6) is indexed as the one-entry pool {1 + 0i} (L = 1, mask 0).
-enum LutMode : int { LUT_WRAP = 0, LUT_POW2 = 1, LUT_GENERAL = 2, LUT_PRNG = 3 /* no pool: ospr.cu */ };
+// LUT_PRNG: no pool, R-5 per draw; LUT_PRNG_TABLE: a draw's top q code bits index a 2^q table (ospr.cu)
+enum LutMode : int { LUT_WRAP = 0, LUT_POW2 = 1, LUT_GENERAL = 2, LUT_PRNG = 3, LUT_PRNG_TABLE = 4 };
 struct LutIndexer {
     uint32_t L;       // N_LUT (> 0)
     uint32_t mode;    // LutMode

@@ -19,9 +19,28 @@ __global__ void __launch_bounds__(256) lut_generate_kernel(uint64_t seed, uint64
         lut[k] = prng_phase(seed, k);
 }
 
+// The sin/cos table of the quantised PRNG source (R-25): entry k = R-5 at the angle code
+// k << (32 - q), i.e. (cos, sin) of 2 pi k / 2^q, for k < 2^q.
+__global__ void __launch_bounds__(256) phase_table_kernel(int q, float2 *tbl)
+{
+    HOLO_PDL_ENTRY();
+    const uint32_t m = 1u << q;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x)
+        tbl[k] = r5_phase(k << (32 - q));
+}
+
 } // namespace holo
 
 using namespace holo;
+
+extern "C" holo_status holo_phase_table(int32_t phase_bits, holo_c64 *table, holo_stream stream)
+{
+    HOLO_CHECK_ARG(phase_bits >= 1 && phase_bits <= 16, "phase_bits must be in [1, 16], got %d", phase_bits);
+    HOLO_CHECK_ARG(table != nullptr, "table is NULL");
+    const unsigned m = 1u << phase_bits, grid = (m + 255) / 256;
+    return launch(K_LUT_GENERATE, phase_table_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, phase_bits,
+                  (float2 *)table);
+}
 
 extern "C" holo_status holo_lut_generate(uint64_t seed, uint64_t n_lut, holo_c64 *lut, holo_stream stream)
 {

@@ -106,26 +106,28 @@ struct RowA {
 // (off + s N^2 + p) mod L) or, in mode LUT_PRNG, SplitMix64 + recipe R-5 evaluated per
 // draw (index off + s N^2 + p, no wrap): bit-identical to a LUT longer than every index.
 struct PhaseSrc {
-    const float2 *lut;
+    const float2 *lut;         // the pool, or (LUT_PRNG_TABLE) the 2^q sin/cos table
     LutIndexer ix;
     uint32_t off_mod, p_mod;   // phase_offset mod L, N^2 mod L
-    uint64_t seed, off;        // LUT_PRNG: stream seed, phase_offset
+    uint64_t seed, off;        // LUT_PRNG(_TABLE): stream seed, phase_offset
+    uint32_t shift;            // LUT_PRNG_TABLE: 32 - q (the table index is the code's top q bits)
 };
 
 template <int N, int LMODE>
 struct PhaseRows {
-    using Base = typename std::conditional<LMODE == LUT_PRNG, uint64_t, uint32_t>::type;
+    static constexpr bool kStream = LMODE == LUT_PRNG || LMODE == LUT_PRNG_TABLE;   // no pool, no wrap
+    using Base = typename std::conditional<kStream, uint64_t, uint32_t>::type;
     // draw index of pixel 0 of global sub-frame s (mod L for the LUT)
     static __device__ __forceinline__ Base subframe(const PhaseSrc &ps, uint64_t s)
     {
-        if constexpr (LMODE == LUT_PRNG)
+        if constexpr (kStream)
             return ps.off + s * (uint64_t)N * N;
         else
             return subframe_base(ps.off_mod, s, ps.p_mod, ps.ix);
     }
     static __device__ __forceinline__ Base row(const PhaseSrc &ps, Base sb, int y)
     {
-        if constexpr (LMODE == LUT_PRNG)
+        if constexpr (kStream)
             return sb + (uint64_t)y * N;
         else
             return row_base(sb, y, N, ps.ix);
@@ -134,6 +136,8 @@ struct PhaseRows {
     {
         if constexpr (LMODE == LUT_PRNG)
             return prng_phase(ps.seed, rb + (uint64_t)x);
+        else if constexpr (LMODE == LUT_PRNG_TABLE)   // PRNG + a small sin/cos table (R-25)
+            return __ldg(ps.lut + ((uint32_t)(splitmix64_at(ps.seed, rb + (uint64_t)x) >> 32) >> ps.shift));
         else
             return __ldg(ps.lut + ps.ix.template mod_t<LMODE>(rb + (uint32_t)x));
     }
@@ -1070,15 +1074,20 @@ holo_status finalize_frame(const float *acc, const float *T, int symmetrise, flo
                   symmetrise, scale, out, om, mse ? parts : (double *)nullptr, counter, 1.0 / cnt, mse);
 }
 
+// The phase source of a call: the pool (a0), SplitMix64 + R-5 per draw (f2), or SplitMix64 +
+// the 2^q-entry sin/cos table (R-25).
+enum PhaseSource : int { SRC_POOL = 0, SRC_PRNG = 1, SRC_TABLE = 2 };
+
 // Pass A over np sub-frame pairs starting at global sub-frame sf_first (ZOUT: the test hook
 // variant that stores conj(Z) instead of its row IFFT).
 template <int N, bool ZOUT>
-static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseSrc &ps, bool prng, uint64_t sf_first,
+static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseSrc &ps, int src, uint64_t sf_first,
                                  int np, int last_has_b, float2 *buf, cudaStream_t s, unsigned *zc = nullptr)
 {
     if constexpr (N >= 1024) {
         using RA2 = RowA2<N>;
-        auto kern = prng                     ? ospr_rows_a2_kernel<N, LUT_PRNG, ZOUT>
+        auto kern = src == SRC_PRNG          ? ospr_rows_a2_kernel<N, LUT_PRNG, ZOUT>
+                  : src == SRC_TABLE         ? ospr_rows_a2_kernel<N, LUT_PRNG_TABLE, ZOUT>
                   : ps.ix.mode == LUT_WRAP ? ospr_rows_a2_kernel<N, LUT_WRAP, ZOUT>
                   : ps.ix.mode == LUT_POW2 ? ospr_rows_a2_kernel<N, LUT_POW2, ZOUT>
                                            : ospr_rows_a2_kernel<N, LUT_GENERAL, ZOUT>;
@@ -1087,7 +1096,8 @@ static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseS
                       Tf, ps, sf_first, np, last_has_b, buf, zc);
     } else {
         using RA = RowA<N>;
-        auto kern = prng                     ? ospr_rows_a_kernel<N, LUT_PRNG, ZOUT>
+        auto kern = src == SRC_PRNG          ? ospr_rows_a_kernel<N, LUT_PRNG, ZOUT>
+                  : src == SRC_TABLE         ? ospr_rows_a_kernel<N, LUT_PRNG_TABLE, ZOUT>
                   : ps.ix.mode == LUT_WRAP ? ospr_rows_a_kernel<N, LUT_WRAP, ZOUT>
                   : ps.ix.mode == LUT_POW2 ? ospr_rows_a_kernel<N, LUT_POW2, ZOUT>
                                            : ospr_rows_a_kernel<N, LUT_GENERAL, ZOUT>;
@@ -1098,13 +1108,17 @@ static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseS
 }
 
 // The phase source of a call (host side).
-static holo_status make_phase_src(int n, const float2 *lut, uint64_t n_lut, bool prng, uint64_t seed,
+// src = SRC_TABLE: lut is the 2^q sin/cos table and n_lut = q (the phase bits).
+static holo_status make_phase_src(int n, const float2 *lut, uint64_t n_lut, int src, uint64_t seed,
                                   uint64_t phase_offset, PhaseSrc *ps)
 {
     const uint64_t P = (uint64_t)n * n;
+    ps->shift = src == SRC_TABLE ? 32u - (uint32_t)n_lut : 0u;
+    if (src != SRC_POOL)
+        n_lut = 0;
     ps->ix = LutIndexer::make(n_lut ? (uint32_t)n_lut : 1u, n);
     ps->lut = lut;                      // N_LUT = 0: the one-entry pool {1 + 0i} (L = 1, R-6)
-    if (lut == nullptr && !prng)
+    if (lut == nullptr && src == SRC_POOL)
         HOLO_TRY(flat_lut(&ps->lut));
     ps->off_mod = n_lut ? (uint32_t)(phase_offset % n_lut) : 0u;
     ps->p_mod = n_lut ? (uint32_t)(P % n_lut) : 0u;
@@ -1115,7 +1129,7 @@ static holo_status make_phase_src(int n, const float2 *lut, uint64_t n_lut, bool
 
 template <int N>
 static holo_status ospr_run(const float2 *tw, const float *target, int n_frames, int n_sub, const float2 *lut, uint64_t n_lut,
-                            bool prng, uint64_t seed, uint64_t phase_offset, int sf_begin, int sf_end,
+                            int src, uint64_t seed, uint64_t phase_offset, int sf_begin, int sf_end,
                             uint8_t *holo_bits, float *intensity, double *mse, holo_region om, void *ws, cudaStream_t s)
 {
     constexpr size_t P = (size_t)N * N;
@@ -1126,7 +1140,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     const int npairs_total = (nsh + 1) / 2;
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     PhaseSrc ps;
-    HOLO_TRY(make_phase_src(N, lut, n_lut, prng, seed, phase_offset, &ps));
+    HOLO_TRY(make_phase_src(N, lut, n_lut, src, seed, phase_offset, &ps));
     // a7 fused into the last chunk's pass C when one warp owns a row (N >= 1024); else its own kernel
     constexpr bool kFuse = RowC<N>::GPW == 1;
     const float scale = full ? 0.5f / (float)n_sub : 0.5f;
@@ -1141,7 +1155,7 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
             const bool last = c0 + np >= npairs_total;
             {
                 const uint64_t sf_first = (uint64_t)f * n_sub + (uint64_t)sf_begin + 2 * (uint64_t)c0;
-                HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, prng, sf_first, np, last_has_b, w.buf, s,
+                HOLO_TRY((launch_pass_a<N, false>(tw, Tf, ps, src, sf_first, np, last_has_b, w.buf, s,
                                                   (kFuse && last) ? cf_ticket : nullptr)));
             }
             typename OsprColBody<N>::Args ca{tw, w.buf, bt, np, last_has_b};
@@ -1213,7 +1227,7 @@ extern "C" int32_t holo_ospr_chunk_pairs(int32_t n, int32_t n_sub)
 }
 
 static holo_status ospr_entry(const float *target, int32_t n, int32_t n_frames, int32_t n_sub, const holo_c64 *lut,
-                              uint64_t n_lut, bool prng, uint64_t seed, uint64_t phase_offset, int32_t sf_begin,
+                              uint64_t n_lut, int src, uint64_t seed, uint64_t phase_offset, int32_t sf_begin,
                               int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse, holo_region omega,
                               void *ws, size_t ws_bytes, holo_stream stream)
 {
@@ -1222,7 +1236,10 @@ static holo_status ospr_entry(const float *target, int32_t n, int32_t n_frames, 
     HOLO_CHECK_ARG(0 <= sf_begin && sf_begin < sf_end && sf_end <= n_sub,
                    "sub-frame range [%d,%d) must be a non-empty part of [0,%d)", sf_begin, sf_end, n_sub);
     HOLO_CHECK_ARG(n_lut < (1ull << 31), "n_lut must be < 2^31");
-    HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
+    if (src == SRC_TABLE)
+        HOLO_CHECK_ARG(lut != nullptr && n_lut >= 1 && n_lut <= 16, "the sin/cos table is required, phase_bits in [1, 16]");
+    else
+        HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
     HOLO_CHECK_ARG(target != nullptr && intensity != nullptr, "target and intensity are required");
     const bool full = (sf_begin == 0 && sf_end == n_sub);
     HOLO_CHECK_ARG(full || mse == nullptr, "mse must be NULL for a partial sub-frame range");
@@ -1237,7 +1254,7 @@ static holo_status ospr_entry(const float *target, int32_t n, int32_t n_frames, 
     const float2 *l = (const float2 *)lut;
 #define HOLO_OSPR_CASE(NN)                                                                                 \
     case NN:                                                                                               \
-        return ospr_run<NN>(tw, target, n_frames, n_sub, l, n_lut, prng, seed, phase_offset, sf_begin, sf_end, \
+        return ospr_run<NN>(tw, target, n_frames, n_sub, l, n_lut, src, seed, phase_offset, sf_begin, sf_end, \
                             holo_bits, intensity, mse, omega, ws, s);
     switch (n) {
         HOLO_OSPR_CASE(16)
@@ -1260,7 +1277,7 @@ extern "C" holo_status holo_ospr_generate(const float *target, int32_t n, int32_
                                           float *intensity, double *mse, holo_region omega, void *ws,
                                           size_t ws_bytes, holo_stream stream)
 {
-    return ospr_entry(target, n, n_frames, n_sub, lut, n_lut, false, 0, phase_offset, sf_begin, sf_end, holo_bits,
+    return ospr_entry(target, n, n_frames, n_sub, lut, n_lut, SRC_POOL, 0, phase_offset, sf_begin, sf_end, holo_bits,
                       intensity, mse, omega, ws, ws_bytes, stream);
 }
 
@@ -1269,8 +1286,19 @@ extern "C" holo_status holo_ospr_generate_prng(const float *target, int32_t n, i
                                                int32_t sf_end, uint8_t *holo_bits, float *intensity, double *mse,
                                                holo_region omega, void *ws, size_t ws_bytes, holo_stream stream)
 {
-    return ospr_entry(target, n, n_frames, n_sub, nullptr, 0, true, seed, phase_offset, sf_begin, sf_end, holo_bits,
+    return ospr_entry(target, n, n_frames, n_sub, nullptr, 0, SRC_PRNG, seed, phase_offset, sf_begin, sf_end, holo_bits,
                       intensity, mse, omega, ws, ws_bytes, stream);
+}
+
+extern "C" holo_status holo_ospr_generate_prng_table(const float *target, int32_t n, int32_t n_frames, int32_t n_sub,
+                                                     uint64_t seed, const holo_c64 *table, int32_t phase_bits,
+                                                     uint64_t phase_offset, int32_t sf_begin, int32_t sf_end,
+                                                     uint8_t *holo_bits, float *intensity, double *mse,
+                                                     holo_region omega, void *ws, size_t ws_bytes, holo_stream stream)
+{
+    HOLO_CHECK_ARG(phase_bits >= 1 && phase_bits <= 16, "phase_bits must be in [1, 16], got %d", phase_bits);
+    return ospr_entry(target, n, n_frames, n_sub, table, (uint64_t)phase_bits, SRC_TABLE, seed, phase_offset,
+                      sf_begin, sf_end, holo_bits, intensity, mse, omega, ws, ws_bytes, stream);
 }
 
 extern "C" holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int32_t n_sub, const holo_c64 *lut,
@@ -1283,20 +1311,24 @@ extern "C" holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int
     HOLO_CHECK_ARG(n_sub >= 1 && 0 <= sf_begin && sf_begin < sf_end && sf_end <= n_sub,
                    "sub-frame range [%d,%d) must be a non-empty part of [0,%d)", sf_begin, sf_end, n_sub);
     HOLO_CHECK_ARG(n_lut < (1ull << 31), "n_lut must be < 2^31");
-    HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
-    HOLO_CHECK_ARG(!use_prng || lut == nullptr, "use_prng excludes a LUT");
+    HOLO_CHECK_ARG(use_prng >= 0 && use_prng <= 2, "use_prng must be 0 (pool), 1 (on the fly) or 2 (table)");
+    if (use_prng == SRC_TABLE)
+        HOLO_CHECK_ARG(lut != nullptr && n_lut >= 1 && n_lut <= 16, "table mode: lut = the table, n_lut = phase_bits");
+    else
+        HOLO_CHECK_ARG((lut == nullptr) == (n_lut == 0), "lut must be NULL iff n_lut == 0");
+    HOLO_CHECK_ARG(use_prng != SRC_PRNG || lut == nullptr, "use_prng excludes a LUT");
     const float2 *tw = nullptr;
     HOLO_TRY(fft::twiddles(&tw));
-    const bool prng = use_prng != 0;
+    const int src = use_prng;
     PhaseSrc ps;
-    HOLO_TRY(make_phase_src(n, (const float2 *)lut, n_lut, prng, prng_seed, phase_offset, &ps));
+    HOLO_TRY(make_phase_src(n, (const float2 *)lut, n_lut, src, prng_seed, phase_offset, &ps));
     const int npairs = (sf_end - sf_begin + 1) / 2;
     const int last_has_b = (sf_begin + 2 * (npairs - 1) + 1) < sf_end;
     cudaStream_t s = (cudaStream_t)stream;
     float2 *z = (float2 *)z_out;
 #define HOLO_PAIRS_CASE(NN)                                                                                  \
     case NN:                                                                                                 \
-        return launch_pass_a<NN, true>(tw, target, ps, prng, (uint64_t)sf_begin, npairs, last_has_b, z, s);
+        return launch_pass_a<NN, true>(tw, target, ps, src, (uint64_t)sf_begin, npairs, last_has_b, z, s);
     switch (n) {
         HOLO_PAIRS_CASE(16)
         HOLO_PAIRS_CASE(32)

@@ -97,6 +97,53 @@ def test_pass_a_pairs_prng_match_oracle(n, offset):
         assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, s)
 
 
+@pytest.mark.parametrize("q", [1, 2, 8, 12, 16])
+def test_phase_table_matches_recipe(q):
+    """holo_phase_table: entry k is recipe R-5 at the code k << (32 - q), rounded to fp32 with
+    -0 -> +0 (R-5 steps 5-6), bit for bit against the oracle's recipe."""
+    tbl = to_np(hb.phase_table(q))
+    codes = (np.arange(1 << q, dtype=np.uint64) << np.uint64(32 - q)).astype(np.uint32)
+    ref = oracle.phase_f64(codes).astype(np.float32)
+    ref[ref == 0] = 0.0                                   # -0 -> +0
+    assert np.array_equal(tbl.real.view(np.uint32), ref[:, 0].view(np.uint32))
+    assert np.array_equal(tbl.imag.view(np.uint32), ref[:, 1].view(np.uint32))
+
+
+@pytest.mark.parametrize("n,q,offset", [(64, 8, 0), (64, 2, 977), (256, 12, 3 << 33), (1024, 16, 5)])
+def test_pass_a_pairs_prng_table_match_oracle(n, q, offset):
+    """P:170 / R-25: pass A with the PRNG + 2^q sin/cos table source equals the oracle's
+    quantised source (apply_phase_prng_q) to fp32 rounding."""
+    T = blobs_target(91 + n, n, 6, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n))
+    S, seed = 3, 2004
+    Z = to_np(hb.debug_ospr_pairs(cuda_target(T), S, None, offset, (0, S), prng_seed=seed, phase_bits=q))
+    P = n * n
+    for j, s in enumerate(range(0, S, 2)):
+        Ra = oracle.apply_phase_prng_q(T, seed, offset + s * P, q)
+        Rb = oracle.apply_phase_prng_q(T, seed, offset + (s + 1) * P, q) if s + 1 < S else np.zeros_like(Ra)
+        ref = np.conj((Ra + np.conj(_mirror(Ra))) + 1j * (Rb + np.conj(_mirror(Rb))))
+        assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, q, s)
+
+
+@pytest.mark.parametrize("n,S,q", [(64, 5, 8), (256, 4, 12), (1024, 6, 16)])
+def test_ospr_prng_table_against_oracle(n, S, q):
+    """The whole OSPR path with the table source: bits against the oracle's fp64 IDFT of its
+    quantised-source randomisation (P-3 band), intensity conditional on the GPU bits (P-4),
+    MSE against the oracle's own bits (P-5)."""
+    T = blobs_target(17, n, 6, max(1.0, n / 16), max(2.0, n / 6), Region.upper_half(n))
+    seed, off = 2004, 4242
+    res = hb.ospr_generate(cuda_target(T), S, prng_seed=seed, phase_bits=q, phase_offset=off)
+    bits = to_np(res.bits)[0]
+    ref_bits = []
+    for s in range(S):
+        h_re = oracle.fft2(oracle.apply_phase_prng_q(T, seed, off + s * n * n, q), True).real
+        check_bits(bits[s], h_re, n)
+        ref_bits.append(oracle.pack_bits((h_re >= 0).astype(np.uint8)))
+    check_intensity(to_np(res.intensity)[0], oracle.replay_from_bits(bits, n))
+    I_ref = oracle.replay_from_bits(np.stack(ref_bits), n)
+    m_ref = oracle.mse_m1(I_ref, T, Region.upper_half(n).as_tuple())
+    assert rel(to_np(res.mse)[0], m_ref) <= REL_TOL
+
+
 # ---- unitary DFT hook ------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048])
