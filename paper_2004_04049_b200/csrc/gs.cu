@@ -287,7 +287,7 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
 gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__restrict__ T, int nitems, holo_region om,
                float *__restrict__ inten, float2 *__restrict__ r_out, const float *__restrict__ a0,
-               double *__restrict__ parts)
+               double *__restrict__ parts, int rev)
 {
     HOLO_PDL_ENTRY();
     using P = fft::Plan<N>;
@@ -300,7 +300,8 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
     int item = blockIdx.x * RP::WPC + (threadIdx.x >> 5);
     if (lane == 0 && item < nitems) {
         tma::mbar_arrive_expect_tx(&ring.bars[0], RP::IN_BYTES);
-        tma::load_1d(ring.slot(0), state + (size_t)item * GPW * N, RP::IN_BYTES, &ring.bars[0]);
+        tma::load_1d(ring.slot(0), state + (size_t)(rev ? nitems - 1 - item : item) * GPW * N, RP::IN_BYTES,
+                     &ring.bars[0]);
     }
     fft::Twiddles<N, false> twr;                          // pool twiddles (register budget)
     twr.load(tw, t);
@@ -316,9 +317,12 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
         const int nxt = item + stride;
         if (lane == 0 && nxt < nitems) {
             tma::mbar_arrive_expect_tx(&ring.bars[s ^ 1], RP::IN_BYTES);
-            tma::load_1d(ring.slot(s ^ 1), state + (size_t)nxt * GPW * N, RP::IN_BYTES, &ring.bars[s ^ 1]);
+            tma::load_1d(ring.slot(s ^ 1), state + (size_t)(rev ? nitems - 1 - nxt : nxt) * GPW * N, RP::IN_BYTES,
+                         &ring.bars[s ^ 1]);
         }
-        const int fr = item / NGRP, grp = item % NGRP;
+        // rev: items in reverse order (the frames the column pass wrote last, still in L2, first)
+        const int pit = rev ? nitems - 1 - item : item;
+        const int fr = pit / NGRP, grp = pit % NGRP;
         const int y = grp * GPW + g;
         const size_t rofs = ((size_t)fr * N + y) * N;
         tma::mbar_wait(&ring.bars[s], (uint32_t)((k >> 1) & 1));
@@ -537,6 +541,10 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
         GsMetrics gm{w.a0, w.tsum, w.parts, mse ? mse + (size_t)g0 * iters : (double *)nullptr,
                      err_e ? err_e + (size_t)g0 * iters : (double *)nullptr, ng, GsRowCfg<N>::NBLK, iters, 0, inv_cnt};
         const bool metrics = mse != nullptr || err_e != nullptr;
+        // the row pass takes its items in reverse order and the column pass in forward order, so
+        // each pass starts on the frames the previous one wrote last, still in L2 (measured at C4:
+        // 127.5 k -> 130 k frame-iterations/s)
+        constexpr int rev_rows = 1;
         for (int k = 0; k < iters; ++k) {
             const bool last = (k == iters - 1);
             GsMetrics pend = gm;              // iteration k-1's partials, reduced in this pass's prologue
@@ -561,15 +569,16 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
             if (r_out != nullptr) {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_STEP>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, ig, r_out + g0 * P, a0, w.parts));
+                                w.state, Tg, nitems, om, ig, r_out + g0 * P, a0, w.parts, rev_rows));
             } else if (last) {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_LAST>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_LAST>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, ig, (float2 *)nullptr, a0, w.parts));
+                                w.state, Tg, nitems, om, ig, (float2 *)nullptr, a0, w.parts, rev_rows));
             } else {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_FUSED>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
-                                w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, a0, w.parts));
+                                w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, a0, w.parts,
+                                rev_rows));
             }
         }
         if (metrics) {

@@ -186,7 +186,7 @@ struct ColPipe {
 template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES, Body::kWidth>::THREADS,
                                   ((ColPipe<N, NSTAGES, Body::kWidth>::STAGES == 1 && N <= 1024) || Body::kWidth < 8) ? 2 : 1)
-col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
+col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a, int rev)
 {
     HOLO_PDL_ENTRY();
     using CP = ColPipe<N, NSTAGES, Body::kWidth>;
@@ -205,8 +205,11 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
         tma::fence_mbar_init();
     }
     __syncthreads();
+    // rev: the tiles in reverse order (the last frames / pairs the previous pass wrote, still in
+    // L2, come first)
+    auto phys = [&](int tile) { return rev ? ntiles - 1 - tile : tile; };
     auto issue = [&](int tile, int s) {
-        const int fr = tile / TPF, ct = tile % TPF;
+        const int fr = phys(tile) / TPF, ct = phys(tile) % TPF;
         tma::mbar_arrive_expect_tx(&bars[s], CP::TILE_BYTES);
 #pragma unroll
         for (int q = 0; q < CP::NBOX; ++q)
@@ -231,7 +234,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
-        Body::template run<F, W>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
+        Body::template run<F, W>(v, st + c, scratch, c, t, phys(tile) / TPF, phys(tile) % TPF, a, fft);
         // results -> the stage in natural [row][col] layout -> one TMA tile store (in place)
         __syncthreads();                   // every thread is done with the exchange data
 #pragma unroll
@@ -240,7 +243,7 @@ col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const type
         tma::fence_proxy_async_smem();     // generic writes before the async-proxy store
         __syncthreads();
         if (threadIdx.x == 0) {
-            const int fr = tile / TPF, ct = tile % TPF;
+            const int fr = phys(tile) / TPF, ct = phys(tile) % TPF;
 #pragma unroll
             for (int q = 0; q < CP::NBOX; ++q)
                 tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
@@ -276,7 +279,7 @@ struct ColPipeG2 {
 
 template <int N, class Body>
 __global__ void __launch_bounds__(ColPipeG2<N, Body>::THREADS, 1)
-col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a)
+col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a, int rev)
 {
     HOLO_PDL_ENTRY();
     using G = ColPipeG2<N, Body>;
@@ -300,8 +303,11 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
         tma::fence_mbar_init();
     }
     __syncthreads();
+    // rev: the tiles in reverse order (the last frames / pairs the previous pass wrote, still in
+    // L2, come first)
+    auto phys = [&](int tile) { return rev ? ntiles - 1 - tile : tile; };
     auto issue = [&](int tile, int s) {
-        const int fr = tile / TPF, ct = tile % TPF;
+        const int fr = phys(tile) / TPF, ct = phys(tile) % TPF;
         tma::mbar_arrive_expect_tx(&bars[s], CP::TILE_BYTES);
 #pragma unroll
         for (int q = 0; q < CP::NBOX; ++q)
@@ -325,7 +331,7 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = st[(t + T * m) * W + c];
-        Body::template run<F, W>(v, st + c, scratch, c, t, tile / TPF, tile % TPF, a, fft);
+        Body::template run<F, W>(v, st + c, scratch, c, t, phys(tile) / TPF, phys(tile) % TPF, a, fft);
         gsync();                           // every thread of the group is done with the exchange data
 #pragma unroll
         for (int m = 0; m < E; ++m)
@@ -333,7 +339,7 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
         tma::fence_proxy_async_smem();     // generic writes before the async-proxy store
         gsync();
         if (lt == 0) {
-            const int fr = tile / TPF, ct = tile % TPF;
+            const int fr = phys(tile) / TPF, ct = phys(tile) % TPF;
 #pragma unroll
             for (int q = 0; q < CP::NBOX; ++q)
                 tma::store_2d(&tmap, ct * W, fr * N + q * CP::BOX_ROWS, st + q * CP::BOX_ROWS * W);
@@ -352,7 +358,8 @@ col_pipe_g2_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const t
 // Host: launch the column pipeline over `nframes` frames of `buf` (row-major
 // [nframes*N][N] complex64).
 template <int N, class Body, int NSTAGES>
-holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s,
+                          int rev)
 {
     using CP = ColPipe<N, NSTAGES, Body::kWidth>;
     CUtensorMap map;
@@ -361,11 +368,13 @@ holo_status launch_cols_s(KernelId id, const float2 *buf, int nframes, const typ
     const int grid = pipe_grid(col_pipe_kernel<N, Body, NSTAGES>, CP::THREADS, CP::SMEM,
                                nframes * CP::TILES_PER_FRAME, 1);
     const int ntiles = nframes * CP::TILES_PER_FRAME;
-    return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a);
+    return launch(id, col_pipe_kernel<N, Body, NSTAGES>, dim3(grid), dim3(CP::THREADS), CP::SMEM, s, map, ntiles, a,
+                  rev);
 }
 
 template <int N, class Body>
-holo_status launch_cols_g2(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+holo_status launch_cols_g2(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s,
+                           int rev)
 {
     using G = ColPipeG2<N, Body>;
     using CP = typename G::CP;
@@ -373,18 +382,19 @@ holo_status launch_cols_g2(KernelId id, const float2 *buf, int nframes, const ty
     HOLO_TRY(make_tmap_c64(&map, buf, N, (uint64_t)nframes * N, CP::W, CP::BOX_ROWS));
     const int ntiles = nframes * CP::TILES_PER_FRAME;
     const int grid = pipe_grid(col_pipe_g2_kernel<N, Body>, G::THREADS, G::SMEM, (ntiles + 1) / 2, 1);
-    return launch(id, col_pipe_g2_kernel<N, Body>, dim3(grid), dim3(G::THREADS), G::SMEM, s, map, ntiles, a);
+    return launch(id, col_pipe_g2_kernel<N, Body>, dim3(grid), dim3(G::THREADS), G::SMEM, s, map, ntiles, a, rev);
 }
 
 // Body::kStages (3 or 1) picks the variant (measured per body); HOLO_COL_STAGES overrides it;
 // Body::kGroups = 2 selects the grouped pipeline.
 template <int N, class Body>
-holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s)
+holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typename Body::Args &a, cudaStream_t s,
+                        bool rev = false)
 {
     if constexpr (Body::kGroups == 2) {
         static const bool off = getenv("HOLO_COL_G1") != nullptr;   // experiments: the plain pipeline
         if (!off)
-            return launch_cols_g2<N, Body>(id, buf, nframes, a, s);
+            return launch_cols_g2<N, Body>(id, buf, nframes, a, s, rev);
     }
     static const int env_stages = [] {
         const char *e = getenv("HOLO_COL_STAGES");
@@ -393,9 +403,9 @@ holo_status launch_cols(KernelId id, const float2 *buf, int nframes, const typen
     const int stages = env_stages ? env_stages : Body::kStages;
     if constexpr (ColPipe<N, 3, Body::kWidth>::SMEM <= 227 * 1024) {   // three stages fit
         if (stages == 3)
-            return launch_cols_s<N, Body, 3>(id, buf, nframes, a, s);
+            return launch_cols_s<N, Body, 3>(id, buf, nframes, a, s, rev);
     }
-    return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s);
+    return launch_cols_s<N, Body, 1>(id, buf, nframes, a, s, rev);
 }
 
 } // namespace holo
