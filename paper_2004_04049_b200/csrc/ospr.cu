@@ -475,6 +475,13 @@ struct OsprColBody {
                     const uint4 *q4 = reinterpret_cast<const uint4 *>(sw + (f * R1 + tt) * W);
                     const uint4 lo = q4[0], hi = q4[1];
                     q[0] = lo.x, q[1] = lo.y, q[2] = lo.z, q[3] = lo.w, q[4] = hi.x, q[5] = hi.y, q[6] = hi.z, q[7] = hi.w;
+                } else if constexpr (sizeof(Word) == 4 && W == 4) {   // one 16-byte load (no 4-way conflict)
+                    const uint4 q4 = *reinterpret_cast<const uint4 *>(sw + (f * R1 + tt) * W);
+                    q[0] = q4.x, q[1] = q4.y, q[2] = q4.z, q[3] = q4.w;
+                } else if constexpr (sizeof(Word) == 8 && W == 4) {   // two 16-byte loads
+                    const ulonglong2 *q2 = reinterpret_cast<const ulonglong2 *>(sw + (f * R1 + tt) * W);
+                    const ulonglong2 lo = q2[0], hi = q2[1];
+                    q[0] = lo.x, q[1] = lo.y, q[2] = hi.x, q[3] = hi.y;
                 } else {
 #pragma unroll
                     for (int cc = 0; cc < W; ++cc)
@@ -725,13 +732,24 @@ struct RowCF {
     using P = fft::Plan<N>;
     static_assert(32 / P::T == 1, "one row per warp");
     static constexpr int NU = N / 2, THREADS = 128;
+    // pair-row slots per warp.  One: four CTAs per SM, so the 512 units of N = 1024 run in one
+    // wave.  Two (HOLO_CF_SLOTS=2, N <= 1024) keep two loads in flight per warp but leave three
+    // CTAs per SM, and the 512 units take 1.15 waves: measured 36.3 vs 33.3 us at C3.
+#ifndef HOLO_CF_SLOTS
+#define HOLO_CF_SLOTS 1
+#endif
+    static constexpr int SLOTS = N <= 1024 ? HOLO_CF_SLOTS : 1;
     static constexpr uint32_t IN_BYTES = (uint32_t)N * 8, SLOT = RowC<N>::SLOT;
-    static constexpr size_t SA = 4 * (size_t)SLOT;                 // A rows ya, yb (fp32)
-    static constexpr size_t SMEM = SA + 2 * (size_t)N * sizeof(float) + 4 * sizeof(uint64_t);
+    // A rows ya, yb (fp32) after the transforms: in the slot memory if it is large enough
+    static constexpr size_t SLOTS_BYTES = 4 * (size_t)SLOTS * SLOT;
+    static constexpr bool A_ALIAS = SLOTS_BYTES >= 2 * (size_t)N * sizeof(float) && SLOTS > 1;
+    static constexpr size_t SA = A_ALIAS ? 0 : SLOTS_BYTES;
+    static constexpr size_t BAR = A_ALIAS ? SLOTS_BYTES : SA + 2 * (size_t)N * sizeof(float);
+    static constexpr size_t SMEM = BAR + 4 * SLOTS * sizeof(uint64_t);
 };
 
 template <int N>
-__global__ void __launch_bounds__(RowCF<N>::THREADS, N <= 1024 ? 4 : 1)   // N = 1024: 512 units in one wave
+__global__ void __launch_bounds__(RowCF<N>::THREADS, N <= 1024 ? 4 - (RowCF<N>::SLOTS - 1) : 1)
 ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
                     const float *__restrict__ acc_in, const float *__restrict__ T, float scale, float *__restrict__ out,
                     holo_region om, double *__restrict__ parts, unsigned *ticket, double inv_count,
@@ -751,21 +769,25 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
     const int u = (int)blockIdx.x;
     const int ya = u, yb = u > 0 ? N - u : N / 2;
     const int y = side ? yb : ya;
-    float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * RC::SLOT);
+    constexpr int NS = RC::SLOTS;
+    float2 *sl0 = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * NS * RC::SLOT);
     float *sA = reinterpret_cast<float *>(smem_raw + RC::SA);           // [2][N]: A of ya, yb
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + RC::SA + 2 * (size_t)N * sizeof(float)) + warp;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + RC::BAR) + warp * NS;
     // T of both rows: read in the epilogue (no registers held across the transforms)
     const int hp = (npairs + 1) / 2, p0 = half * hp, p1 = half ? npairs : hp;
     auto src = [&](int p) { return buf + ((size_t)p * N + (size_t)y) * N; };
+    auto slot = [&](int i) { return sl0 + (size_t)i * (RC::SLOT / sizeof(float2)); };
     if (lane == 0) {
-        tma::mbar_init(bar, 1);
+        for (int i = 0; i < NS; ++i)
+            tma::mbar_init(&bar[i], 1);
         tma::fence_mbar_init();
     }
     __syncwarp();
-    if (lane == 0 && p0 < p1) {
-        tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
-        tma::load_1d(sl, src(p0), RC::IN_BYTES, bar);
-    }
+    if (lane == 0)                       // the first NS pair rows in flight
+        for (int i = 0; i < NS && p0 + i < p1; ++i) {
+            tma::mbar_arrive_expect_tx(&bar[i], RC::IN_BYTES);
+            tma::load_1d(slot(i), src(p0 + i), RC::IN_BYTES, &bar[i]);
+        }
     float a[E];
 #pragma unroll
     for (int r = 0; r < E; ++r)
@@ -773,25 +795,30 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
     uint32_t k = 0;
     #pragma unroll 1
     for (int p = p0; p < p1; ++p, ++k) {
-        tma::mbar_wait(bar, k & 1u);
+        const int si = NS > 1 ? (int)(k % NS) : 0;
+        float2 *sl = slot(si);
+        tma::mbar_wait(&bar[si], (k / NS) & 1u);
         float2 v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)
             v[m] = sl[t + R1 * m];
-        const bool more = p + 1 < p1;
-        const float2 *nx = src(p + 1);
+        const bool more = p + NS < p1;
+        const float2 *nx = src(p + NS);
         fft::fft2pass_hook<N, false, 1, true>(v, sl, t, tw, [&] {
+            // WAR across proxies: the exchange reads of this slot before the TMA refill
             tma::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && more) {
-                tma::mbar_arrive_expect_tx(bar, RC::IN_BYTES);
-                tma::load_1d(sl, nx, RC::IN_BYTES, bar);
+                tma::mbar_arrive_expect_tx(&bar[si], RC::IN_BYTES);
+                tma::load_1d(sl, nx, RC::IN_BYTES, &bar[si]);
             }
         });
 #pragma unroll
         for (int r = 0; r < E; ++r)
             a[r] = __fmaf_rn(v[r].x, v[r].x, __fmaf_rn(v[r].y, v[r].y, a[r]));
     }
+    if constexpr (RC::A_ALIAS)
+        __syncthreads();                 // every warp is done with its slots (sA aliases them)
     // A row = (half 0 + half 1) / N^2 (+ earlier chunks' sums), fixed order as in pass C
     float *rowA = sA + (size_t)side * N;
     if (half == 1) {

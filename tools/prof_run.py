@@ -22,6 +22,14 @@ if what in ("all", "ospr"):
         r = hb.ospr_generate(T, w.n_sub, lut)
     torch.cuda.synchronize()
     print("ospr mse", r.mse.item())
+if what == "c5":
+    w = WORKLOADS["C5"]
+    T = torch.from_numpy(target_for(w)).to(dev)
+    lut = hb.lut_generate(LUT_SEED, 1 << 16)
+    for _ in range(reps):
+        r = hb.ospr_generate(T, w.n_sub, lut)
+    torch.cuda.synchronize()
+    print("c5 mse", r.mse.item())
 if what in ("all", "gs", "gs64"):
     w = WORKLOADS["C4"]
     nfr = w.frames if what == "gs64" else 8          # gs64: the whole C4 launch group (512 MiB state)
