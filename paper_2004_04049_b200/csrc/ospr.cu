@@ -278,8 +278,11 @@ struct RowA2 {
     static constexpr int UNITS_PER_PAIR = N / 2;
 };
 
+#ifndef HOLO_A2_MINB2048
+#define HOLO_A2_MINB2048 3
+#endif
 template <int N, int LMODE, bool ZOUT = false>
-__global__ void __launch_bounds__(RowA2<N>::WPC * 32)
+__global__ void __launch_bounds__(RowA2<N>::WPC * 32, (N == 2048 && HOLO_A2_MINB2048) ? HOLO_A2_MINB2048 : 0)
 ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
                     int npairs, int last_pair_has_b, float2 *__restrict__ buf, unsigned *zc)
 {
@@ -296,11 +299,15 @@ ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
     const int up = warp >> 1, h = warp & 1;                      // unit slot in the CTA, half
     float2 *s0 = reinterpret_cast<float2 *>(smem_raw + (size_t)(2 * up) * RA::SLOT);
     float2 *s1 = reinterpret_cast<float2 *>(smem_raw + (size_t)(2 * up + 1) * RA::SLOT);
-    // N = 1024: pass-2 twiddles factorised into registers (20 instead of 62; no loads per transform:
-    // 42.4 -> 39.9 us at C3); N = 2048 (E = 64): from the L1-resident pool (registers cost warps)
-    using TwSrc = typename std::conditional<(N <= 1024), fft::TwFact<N>, fft::TwGlobal<N>>::type;
+    // pass-2 twiddles factorised into registers (no loads per transform; 20 registers instead of 62
+    // at N = 1024: 42.4 -> 39.9 us at C3; at N = 2048 capped at 168 registers for three CTAs per SM:
+    // C5 0.634 -> 0.620 ms)
+#ifndef HOLO_A2_TWF_MAXN
+#define HOLO_A2_TWF_MAXN 2048
+#endif
+    using TwSrc = typename std::conditional<(N <= HOLO_A2_TWF_MAXN), fft::TwFact<N>, fft::TwGlobal<N>>::type;
     TwSrc twp;
-    if constexpr (N <= 1024)
+    if constexpr (N <= HOLO_A2_TWF_MAXN)
         twp.load(tw, t);
     else
         twp.p = tw + P::TW_OFFSET + t;
@@ -337,13 +344,23 @@ ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
                     S0[0] = z.z1;
                     s1[xm] = z.z2;
                 }
+                if (has_b) {   // (every pair but an unpaired tail: no R_b scaling in the loop)
 #pragma unroll
-                for (int m = 1; m < MH; ++m) {
-                    const float t1 = T1l[32 * m], t2 = T2l[-32 * m];
-                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[32 * m], LA2[-32 * m], LB1[32 * m],
-                                           LB2[-32 * m]);
-                    S0[32 * m] = z.z1;
-                    S1[-32 * m] = z.z2;
+                    for (int m = 1; m < MH; ++m) {
+                        const float t1 = T1l[32 * m], t2 = T2l[-32 * m];
+                        const ZPair z = z_pair(t1, t2, t1, t2, LA1[32 * m], LA2[-32 * m], LB1[32 * m], LB2[-32 * m]);
+                        S0[32 * m] = z.z1;
+                        S1[-32 * m] = z.z2;
+                    }
+                } else {
+#pragma unroll 4
+                    for (int m = 1; m < MH; ++m) {
+                        const float t1 = T1l[32 * m], t2 = T2l[-32 * m];
+                        const ZPair z = z_pair(t1, t2, 0.0f, 0.0f, LA1[32 * m], LA2[-32 * m], LB1[32 * m],
+                                               LB2[-32 * m]);
+                        S0[32 * m] = z.z1;
+                        S1[-32 * m] = z.z2;
+                    }
                 }
             } else {
 #pragma unroll (LMODE == LUT_PRNG ? 2 : 8)
