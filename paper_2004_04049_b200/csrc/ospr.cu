@@ -455,15 +455,34 @@ struct OsprColBody {
             fft.template run<false, W>(v, sm, t);
             if (h == 0) {                                        // v = conj(H) (x N): Re H = v.x, Im H = -v.y
                 // u = (Re H, Im H) + 0 (one FADD2): -0.0 becomes +0.0, so u's sign bit is set iff
-                // the value is < 0, and h' = +-1 is that sign bit on 1.0f (R-7: Re H >= 0 -> +1)
+                // the value is < 0, and h' = +-1 is that sign bit on 1.0f (R-7: Re H >= 0 -> +1).
+                if constexpr (E <= 32) {
+                    // the sign bits are shifted into a 32-bit word by one funnel shift each, last
+                    // element first (bit r = element r), and inverted once at the end (C3: the
+                    // column pass 1328 -> 1232 instructions per thread and tile)
+                    uint32_t sa = 0, sb = 0;
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    const float2 u = f2::add(conjf2(v[r]), make_float2(0.0f, 0.0f));
-                    const uint32_t ua = __float_as_uint(u.x), ub = __float_as_uint(u.y);
-                    wa |= (Word)((~ua) >> 31) << r;
-                    wb |= (Word)((~ub) >> 31) << r;
-                    v[r] = make_float2(__uint_as_float((ua & 0x80000000u) | 0x3f800000u),
-                                       __uint_as_float((ub & 0x80000000u) | 0x3f800000u));
+                    for (int r = E - 1; r >= 0; --r) {
+                        const float2 u = f2::add(conjf2(v[r]), make_float2(0.0f, 0.0f));
+                        const uint32_t ua = __float_as_uint(u.x), ub = __float_as_uint(u.y);
+                        sa = __funnelshift_l(ua, sa, 1);
+                        sb = __funnelshift_l(ub, sb, 1);
+                        v[r] = make_float2(__uint_as_float((ua & 0x80000000u) | 0x3f800000u),
+                                           __uint_as_float((ub & 0x80000000u) | 0x3f800000u));
+                    }
+                    constexpr uint32_t mask = E < 32 ? (1u << E) - 1u : 0xFFFFFFFFu;
+                    wa = (Word)(~sa & mask);
+                    wb = (Word)(~sb & mask);
+                } else {   // E = 64 (N = 2048): per-bit insertion measured faster there (C5 0.616 vs 0.65 ms)
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        const float2 u = f2::add(conjf2(v[r]), make_float2(0.0f, 0.0f));
+                        const uint32_t ua = __float_as_uint(u.x), ub = __float_as_uint(u.y);
+                        wa |= (Word)((~ua) >> 31) << r;
+                        wb |= (Word)((~ub) >> 31) << r;
+                        v[r] = make_float2(__uint_as_float((ua & 0x80000000u) | 0x3f800000u),
+                                           __uint_as_float((ub & 0x80000000u) | 0x3f800000u));
+                    }
                 }
                 if (!has_b) {                                    // unpaired tail: h'_b = 0
 #pragma unroll
