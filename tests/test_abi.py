@@ -156,3 +156,35 @@ def test_plan_queries(L):
     assert L.holo_gs_group_frames(64, 0) == 0
     assert L.holo_ospr_finalize_workspace_size() >= 592 * 5 * 8 + 4
     assert L.holo_ospr_workspace_size(1024, 1, 24) >= L.holo_ospr_finalize_workspace_size()
+
+
+def test_round2_entry_points_arg_errors(L):
+    """The row-slice a7, MSE-from-sums and sin/cos-table entry points validate their arguments on
+    the host (no device work before the checks)."""
+    om = _region(1, 32, 0, 64)
+    fin = L.holo_ospr_finalize_workspace_size()
+    # row slice empty, reversed or outside the frame
+    for r0, r1 in ((5, 5), (9, 3), (-1, 4), (60, 65)):
+        assert L.holo_ospr_finalize_rows(FAKE, FAKE, 64, r0, r1, 8, om, FAKE, FAKE, FAKE, fin, None) == \
+            _lib.HOLO_ERR_INVALID_ARG
+    assert b"row slice" in L.holo_last_error()
+    assert L.holo_ospr_finalize_rows(FAKE, FAKE, 64, 0, 8, 0, om, FAKE, FAKE, FAKE, fin, None) == \
+        _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_finalize_rows(FAKE, FAKE, 64, 0, 8, 8, om, FAKE, None, FAKE, fin, None) == \
+        _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_finalize_rows(FAKE, FAKE, 64, 0, 8, 8, om, FAKE, FAKE, FAKE, fin - 8, None) == \
+        _lib.HOLO_ERR_WORKSPACE
+    assert L.holo_ospr_finalize_rows(FAKE, FAKE, 100, 0, 8, 8, om, FAKE, FAKE, FAKE, fin, None) == \
+        _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_mse_from_sums(None, 1, om, FAKE, None) == _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_mse_from_sums(FAKE, 0, om, FAKE, None) == _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_mse_from_sums(FAKE, 1, _region(3, 3, 0, 8), FAKE, None) == _lib.HOLO_ERR_INVALID_ARG
+    # phase table: 1 <= phase_bits <= 16
+    for q in (0, 17, -3):
+        assert L.holo_phase_table(q, FAKE, None) == _lib.HOLO_ERR_INVALID_ARG
+    assert b"phase_bits" in L.holo_last_error()
+    assert L.holo_phase_table(8, None, None) == _lib.HOLO_ERR_INVALID_ARG
+    ws = L.holo_ospr_workspace_size(64, 1, 8)
+    for q, tbl in ((0, FAKE), (17, FAKE), (8, None)):
+        assert L.holo_ospr_generate_prng_table(FAKE, 64, 1, 8, 7, tbl, q, 0, 0, 8, None, FAKE, FAKE, om, FAKE, ws,
+                                               None) == _lib.HOLO_ERR_INVALID_ARG
