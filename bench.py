@@ -754,7 +754,9 @@ def c5_video(args, hb, world, rank, dev, flush):
                                  "all-reduce of 5 doubles, MSE -- on a side stream overlapping the next frame"
                                  if sworld > 1 else "whole frames on one GPU, fused a7, no collective") +
                                 (" [FAKE: stand-in collectives, not a result]" if fake > 1 else ""),
-                   "l2": "flushed once before each timed run of kf frames", "launch": "eager launches, two streams"},
+                   "l2": "flushed once before each timed run of kf frames; each frame's working set (the "
+                         "512 MiB pair buffer of 16 pairs) exceeds the 126 MB L2",
+                   "launch": "eager launches, two streams"},
     }
 
 
