@@ -29,7 +29,7 @@
  *    interleaved (re, im) fp32 pairs (`holo_c64`); DC is at [0][0] with no
  *    shift (R-10); the DFT pair is unitary, 1/sqrt(Nx*Ny) in both
  *    directions (Eqs. (1)-(2); R-9).
- *  - N (`n`) must be a power of two in [16, 2048] (square frames); other
+ *  - N (`n`) must be a power of two in [16, 4096] (square frames); other
  *    sizes return HOLO_ERR_INVALID_ARG.
  *  - On any status other than HOLO_OK nothing has been enqueued except for
  *    HOLO_ERR_CUDA, which reports a launch failure (some work may have been
@@ -112,7 +112,7 @@ holo_status holo_lut_generate(uint64_t seed, uint64_t n_lut, holo_c64 *lut, holo
  * ("Hermitian pairing"); an odd count leaves one unpaired.
  *
  *   target      [n_frames][n][n] fp32 amplitude T, values in [0, 1] (R-11)
- *   n           N, power of two in [16, 2048]
+ *   n           N, power of two in [16, 4096]
  *   n_frames    >= 1
  *   n_sub       N_SF, sub-frames per frame, >= 1
  *   lut         [n_lut] holo_c64 (NULL iff n_lut == 0)

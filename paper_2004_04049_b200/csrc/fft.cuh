@@ -173,7 +173,7 @@ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
 template <int N>
 struct Plan {
-    static_assert(N >= 16 && N <= 2048 && (N & (N - 1)) == 0, "N must be a power of two in [16, 2048]");
+    static_assert(N >= 16 && N <= 4096 && (N & (N - 1)) == 0, "N must be a power of two in [16, 4096]");
     static constexpr int LOG = ilog2(N);
     static constexpr int R1 = 1 << (LOG / 2);       // threads per transform
     static constexpr int R2 = N / R1;               // values per thread (E)
@@ -186,10 +186,10 @@ struct Plan {
 
 // Pass-2 twiddles: g_tw[TW_OFFSET(N) + r*R1 + t] = W_N^{r*t} (forward sign), r < R2, t < R1.
 // Laid out r-major so that the R1 threads of a transform read consecutive entries.
-// Pool size: sum over N = 16..2048 of N = 4080 entries.  Built once per device by
+// Pool size: sum over N = 16..4096 of N = 8176 entries.  Built once per device by
 // holo::fft::twiddles() (host libm in double, rounded to fp32) in library-owned
 // device memory; kernels receive the pool pointer as an argument.
-constexpr int kTwPool = 4096;   // 4080 two-pass entries (N = 16 .. 2048)
+constexpr int kTwPool = 8192;   // 8176 two-pass entries (N = 16 .. 4096)
 holo_status twiddles(const float2 **pool);
 
 __device__ __forceinline__ int pad_index(int i, int r1) { return i + i / r1; }

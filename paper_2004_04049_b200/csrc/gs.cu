@@ -14,7 +14,7 @@
 //
 // The 1/sqrt(N) factors of the inverse transforms are dropped: the constraint
 // and the amplitude replacement are invariant to a positive scale.
-#include "passes.cuh"
+#include "rows2w.cuh"
 
 namespace holo {
 
@@ -23,7 +23,9 @@ constexpr int kGsParts = 5;   // per-item metric partial sums (gs_rows_kernel)
 
 template <int N>
 struct GsRowCfg {
-    static constexpr int NBLK = N / RowPipe<N>::GPW;   // partial-sum slots per frame and iteration
+    static constexpr bool kWide = fft::Plan<N>::T > 32;   // N = 4096: two warps per row (gs_rows2w_kernel)
+    // partial-sum slots per frame and iteration: one per row item, or (4096) one per warp
+    static constexpr int NBLK = kWide ? 2 * N : N / RowPipe<N>::GPW;
 };
 
 
@@ -186,7 +188,8 @@ gs_mse_kernel(const GsMetrics gm)
 template <int N, bool QUANT>
 struct GsColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
-    static constexpr int kWidth = 8;   // columns per tile (4 measured 6 % slower for this body)
+    // columns per tile (4 measured 6 % slower for this body; N = 4096: 4, one 133 KB stage)
+    static constexpr int kWidth = N >= 4096 ? 4 : 8;
     static constexpr int kGroups = 1;
     static constexpr bool kPrologue = true;
     struct Args {
@@ -414,6 +417,104 @@ gs_rows_kernel(const float2 *__restrict__ tw, float2 *state, const float *__rest
     }
 }
 
+// Row pass for N = 4096 (R-26): a two-warp group per row (item = row, frame-major), rows read and
+// written straight from the state (coalesced).  Same arithmetic per element as gs_rows_kernel;
+// each warp's fp64 partial sums go to its own slot parts[frame][2 y + warp] (NBLK = 2 N).
+template <int N, int MODE>
+__global__ void __launch_bounds__(Row2W<N>::THREADS, 1)
+gs_rows2w_kernel(const float2 *__restrict__ tw, float2 *state, const float *__restrict__ T, int nrows, holo_region om,
+                 float *__restrict__ inten, float2 *__restrict__ r_out, const float *__restrict__ a0,
+                 double *__restrict__ parts, int rev)
+{
+    HOLO_PDL_ENTRY();
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E, NBLK = GsRowCfg<N>::NBLK;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const Row2WThread rt = row2w_thread();
+    float2 *sm = reinterpret_cast<float2 *>(smem_raw) + (size_t)rt.grp * P::SMEM;
+    const int t = rt.t, lane = threadIdx.x & 31, wig = t >> 5;   // warp within the row group
+    constexpr float inv_n = 1.0f / (float)N;
+    static_assert(E <= 64, "one column-mask bit per element");
+    uint64_t colmask = 0;
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        colmask |= (uint64_t)(t + R1 * r >= om.col0 && t + R1 * r < om.col1) << r;
+    #pragma unroll 1
+    for (int item = blockIdx.x * 2 + rt.grp; item < nrows; item += gridDim.x * 2) {
+        const int pit = rev ? nrows - 1 - item : item;
+        const int fr = pit / N, y = pit % N;
+        const size_t rofs = ((size_t)fr * N + y) * N;
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = state[rofs + t + R1 * m];
+        #pragma unroll 1
+        for (int h = 0; h < (MODE == GS_FUSED ? 2 : 1); ++h) {
+            float tv[E];
+            if (h == 0) {
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    tv[r] = __ldg(T + rofs + t + R1 * r);
+            }
+            row2w_fft<N>(v, sm, tw, rt);
+            if (h == 1) {
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    state[rofs + t + R1 * r] = v[r];
+                break;
+            }
+            float fe = 0.0f, sI = 0.0f, sII = 0.0f, sDD = 0.0f, sDI = 0.0f;
+            const float a0n = __fmul_rn(a0[fr], inv_n * inv_n);
+            const uint64_t in_om = (y >= om.row0 && y < om.row1) ? colmask : 0u;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int x = t + R1 * r;
+                const float2 X = v[r];
+                const float m2 = __fmaf_rn(X.x, X.x, __fmul_rn(X.y, X.y));
+                const bool nz = m2 >= kFltMin;
+                const float tt = tv[r];
+                const GsAmp ga = gs_amp(m2, tt, nz);
+                const float d = __fmaf_rn(ga.mag, inv_n, -tt);
+                fe = __fmaf_rn(d, d, fe);
+                if ((in_om >> r) & 1u) {
+                    const float dd = __fmaf_rn(a0n, m2, -__fmul_rn(tt, tt));
+                    sI = __fadd_rn(sI, m2);
+                    sII = __fmaf_rn(m2, m2, sII);
+                    sDD = __fmaf_rn(dd, dd, sDD);
+                    sDI = __fmaf_rn(dd, m2, sDI);
+                }
+                if (MODE == GS_LAST || MODE == GS_STEP) {
+                    if (inten != nullptr)
+                        inten[rofs + x] = __fmul_rn(m2, inv_n * inv_n);
+                }
+                if (MODE != GS_LAST)
+                    v[r] = nz ? f2::mul(conjf2(X), f2::bc(ga.g)) : make_float2(tt, -0.0f);
+            }
+            constexpr double i2 = 1.0 / ((double)N * N), i4 = i2 * i2;
+            double sums[kGsParts] = {(double)sI * i2, (double)sII * i4, (double)sDD, (double)sDI * i2, (double)fe};
+#pragma unroll
+            for (int i = 0; i < kGsParts; ++i) {
+                double x = sums[i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+                    x += __shfl_down_sync(0xffffffffu, x, o);
+                sums[i] = x;
+            }
+            if (lane == 0) {
+                double *dst = parts + ((size_t)fr * NBLK + 2 * y + wig) * kGsParts;
+#pragma unroll
+                for (int i = 0; i < kGsParts; ++i)
+                    dst[i] = sums[i];
+            }
+            if (MODE == GS_STEP) {
+#pragma unroll
+                for (int r = 0; r < E; ++r)
+                    r_out[rofs + t + R1 * r] = conjf2(v[r]);
+            }
+        }
+    }
+}
+
 // One CTA per frame of a launch group: fixed-order sum of the prepare kernel's T partials ->
 // tsum[frame] = (sum T^2, sum T^4) over Omega and the prior a0 = sum T^2 / |Omega| that the
 // row pass takes its metric partials about (exactly R-12's a for the full plane, by Parseval).
@@ -463,7 +564,8 @@ static int gs_nblk(int n)
     case 256: return GsRowCfg<256>::NBLK;
     case 512: return GsRowCfg<512>::NBLK;
     case 1024: return GsRowCfg<1024>::NBLK;
-    default: return GsRowCfg<2048>::NBLK;
+    case 2048: return GsRowCfg<2048>::NBLK;
+    default: return GsRowCfg<4096>::NBLK;
     }
 }
 
@@ -535,7 +637,7 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                         w.tparts));
         HOLO_TRY(launch(K_MSE_REDUCE, gs_tsum_kernel, dim3(ng), dim3(kGsTBlocks), 0, s, (const double *)w.tparts,
                         inv_cnt, w.tsum, w.a0));
-        HOLO_TRY((launch_rows_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));   // F{conj(R_0)}
+        HOLO_TRY((launch_row_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));    // F{conj(R_0)}
         using RP = RowPipe<N>;
         const float *Tg = target + g0 * P;
         GsMetrics gm{w.a0, w.tsum, w.parts, mse ? mse + (size_t)g0 * iters : (double *)nullptr,
@@ -562,10 +664,22 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                                                      pend};
                 HOLO_TRY((launch_cols<N, GsColBody<N, true>>(K_GS_COLS, w.state, ng, ca, s)));
             }
-            constexpr size_t smem = ring_smem<RP::SLOT_C, RP::WPC>();
-            const int nitems = ng * GsRowCfg<N>::NBLK;
             float *ig = intensity ? intensity + g0 * P : (float *)nullptr;
             const float *a0 = w.a0;
+            if constexpr (GsRowCfg<N>::kWide) {
+                using R = Row2W<N>;
+                const int nrows = ng * N;
+                auto kern = r_out != nullptr ? gs_rows2w_kernel<N, GS_STEP>
+                          : last             ? gs_rows2w_kernel<N, GS_LAST>
+                                             : gs_rows2w_kernel<N, GS_FUSED>;
+                const int grid = pipe_grid(kern, R::THREADS, R::SMEM, (nrows + 1) / 2, 1);
+                HOLO_TRY(launch(K_GS_ROWS, kern, dim3(grid), dim3(R::THREADS), R::SMEM, s, tw, w.state, Tg, nrows, om,
+                                (r_out != nullptr || last) ? ig : (float *)nullptr,
+                                r_out ? r_out + g0 * P : (float2 *)nullptr, a0, w.parts, rev_rows));
+                continue;
+            } else {
+            constexpr size_t smem = ring_smem<RP::SLOT_C, RP::WPC>();
+            const int nitems = ng * GsRowCfg<N>::NBLK;
             if (r_out != nullptr) {
                 const int grid = pipe_grid(gs_rows_kernel<N, GS_STEP>, RP::WPC * 32, smem, nitems, RP::WPC);
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_STEP>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
@@ -579,6 +693,7 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
                 HOLO_TRY(launch(K_GS_ROWS, gs_rows_kernel<N, GS_FUSED>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
                                 w.state, Tg, nitems, om, (float *)nullptr, (float2 *)nullptr, a0, w.parts,
                                 rev_rows));
+            }
             }
         }
         if (metrics) {
@@ -607,6 +722,7 @@ static holo_status gs_dispatch(const float2 *tw, int n, const float *target, int
         HOLO_GS_CASE(512)
         HOLO_GS_CASE(1024)
         HOLO_GS_CASE(2048)
+        HOLO_GS_CASE(4096)
     default:
         return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }

@@ -1,14 +1,14 @@
 // hooks.cu -- test hooks of the C ABI (not on the hot path): a plain unitary 2D
 // DFT/IDFT (Eqs. (1)-(2)) built from the same FFT device code as the
 // fused passes, and step a2 (randomisation) alone for bit-exact probing.
-#include "passes.cuh"
+#include "rows2w.cuh"
 
 namespace holo {
 
 template <int N, bool INV>
 struct HookColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
-    static constexpr int kWidth = 8;   // columns per tile
+    static constexpr int kWidth = N >= 4096 ? 4 : 8;   // columns per tile (4096: one 133 KB stage)
     static constexpr int kGroups = 1;
     struct Args {
         const float2 *tw;
@@ -34,11 +34,11 @@ static holo_status fft2_run(const float2 *tw, const float2 *in, float2 *out, int
     const int nrows = batch * N;
     const float scale = 1.0f / (float)N;   // unitary: 1/sqrt(N*N), an exact power of two
     if (inverse) {
-        HOLO_TRY((launch_rows_fft<N, true>(K_FFT_ROWS, tw, in, out, nrows, s)));
+        HOLO_TRY((launch_row_fft<N, true>(K_FFT_ROWS, tw, in, out, nrows, s)));
         typename HookColBody<N, true>::Args a{tw, out, scale};
         HOLO_TRY((launch_cols<N, HookColBody<N, true>>(K_FFT_COLS, out, batch, a, s)));
     } else {
-        HOLO_TRY((launch_rows_fft<N, false>(K_FFT_ROWS, tw, in, out, nrows, s)));
+        HOLO_TRY((launch_row_fft<N, false>(K_FFT_ROWS, tw, in, out, nrows, s)));
         typename HookColBody<N, false>::Args a{tw, out, scale};
         HOLO_TRY((launch_cols<N, HookColBody<N, false>>(K_FFT_COLS, out, batch, a, s)));
     }
@@ -87,6 +87,7 @@ extern "C" holo_status holo_fft2(const holo_c64 *in, holo_c64 *out, int32_t n, i
     case 512: return fft2_run<512>(tw, i, o, batch, inverse, s);
     case 1024: return fft2_run<1024>(tw, i, o, batch, inverse, s);
     case 2048: return fft2_run<2048>(tw, i, o, batch, inverse, s);
+    case 4096: return fft2_run<4096>(tw, i, o, batch, inverse, s);
     default: return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }
 }

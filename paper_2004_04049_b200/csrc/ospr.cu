@@ -27,6 +27,7 @@
 
 #include "passes.cuh"
 #include "phase.cuh"
+#include "rows2w.cuh"
 
 namespace holo {
 
@@ -404,6 +405,89 @@ ospr_rows_a2_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
     }
 }
 
+// Pass A for N = 4096 (a row transform spans two warps, R-26): one CTA of four warps per unit
+// {y, N - y}.  All four warps build Z for the unit's pixel pairs (a quarter of the columns
+// each) into two row slots, then warps 0-1 row-IFFT row y and warps 2-3 row N - y, each pair
+// on its own named barrier.  Same phase indexing and Z arithmetic as ospr_rows_a2_kernel.
+template <int N>
+struct RowA4 {
+    using P = fft::Plan<N>;
+    static_assert(P::T == 64, "two warps per row");
+    static constexpr int THREADS = 128;
+    static constexpr uint32_t SLOT = ((uint32_t)P::SMEM * 8 + 127) / 128 * 128;   // one row
+    static constexpr size_t SMEM = 2 * (size_t)SLOT;
+    static constexpr int UNITS_PER_PAIR = N / 2;
+};
+
+template <int N, int LMODE, bool ZOUT = false>
+__global__ void __launch_bounds__(RowA4<N>::THREADS, 1)
+ospr_rows_a4_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
+                    int npairs, int last_pair_has_b, float2 *__restrict__ buf)
+{
+    HOLO_PDL_ENTRY();
+    using P = fft::Plan<N>;
+    using RA = RowA4<N>;
+    using PR = PhaseRows<N, LMODE>;
+    using Base = typename PR::Base;
+    constexpr int R1 = P::R1, E = P::E;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *s0 = reinterpret_cast<float2 *>(smem_raw);
+    float2 *s1 = reinterpret_cast<float2 *>(smem_raw + RA::SLOT);
+    const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63;
+    const fft::GroupSync gsync{1 + grp, 64};
+    const int nunits = npairs * RA::UNITS_PER_PAIR;
+    #pragma unroll 1
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int pair = u / RA::UNITS_PER_PAIR, k = u % RA::UNITS_PER_PAIR;
+        const bool has_b = (pair < npairs - 1) || last_pair_has_b;
+        const Base ba = PR::subframe(ps, sf_first + 2 * (uint64_t)pair);
+        const Base bb = PR::subframe(ps, sf_first + 2 * (uint64_t)pair + 1);
+        const float bsc = has_b ? 1.0f : 0.0f;   // an absent sub-frame b contributes R_b = 0
+        const int y = k, ym = k > 0 ? N - k : N / 2;
+        if (k > 0) {   // pixel pairs (y, x) <-> (ym, N - x) for every x
+            const Base a1 = PR::row(ps, ba, y), a2 = PR::row(ps, ba, ym);
+            const Base b1 = PR::row(ps, bb, y), b2 = PR::row(ps, bb, ym);
+            const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
+#pragma unroll 4
+            for (int x = tid; x < N; x += RA::THREADS) {
+                const int xm = (N - x) & (N - 1);
+                const float t1 = T1[x], t2 = T2[xm];
+                const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a2, xm),
+                                       PR::at(ps, b1, x), PR::at(ps, b2, xm));
+                s0[x] = z.z1;
+                s1[xm] = z.z2;
+            }
+        } else {       // unit 0: rows 0 and N/2, each its own mirror; group grp builds row grp
+            const int yy = grp ? N / 2 : 0;
+            float2 *d = grp ? s1 : s0;
+            const Base a1 = PR::row(ps, ba, yy), b1 = PR::row(ps, bb, yy);
+            const float *T1 = T + (size_t)yy * N;
+            for (int x = t; x <= N / 2; x += 64) {
+                const int xm = (N - x) & (N - 1);
+                const float t1 = T1[x], t2 = T1[xm];
+                const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a1, xm),
+                                       PR::at(ps, b1, x), PR::at(ps, b1, xm));
+                d[x] = z.z1;
+                d[xm] = z.z2;
+            }
+        }
+        __syncthreads();                                     // Z of both rows is built
+        float2 *sg = grp ? s1 : s0;
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            v[m] = sg[t + R1 * m];                           // conj(Z), built so by the producer
+        if constexpr (!ZOUT)                                 // ZOUT: the test hook writes conj(Z) itself
+            fft::fft2pass_impl<N, false, 1, false>(v, sg, t, fft::TwGlobal<N>{tw + P::TW_OFFSET + t}, fft::NoHook(),
+                                                   gsync);
+        float2 *o = buf + ((size_t)pair * N + (grp ? ym : y)) * N;
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            o[t + R1 * m] = v[m];       // conj of the row IFFT (the pair buffer is kept conjugated)
+        __syncthreads();                                     // both slots read before the next unit
+    }
+}
+
 // ---- pass B: column IFFT -> a4 sign + pack -> column FFT (TMA-fed pipeline) ------------------
 // 8x8 bit-matrix transpose (bit 8i + j <-> bit 8j + i), three masked swap stages.
 __device__ __forceinline__ uint64_t transpose8x8(uint64_t x)
@@ -427,7 +511,8 @@ struct OsprColBody {
     // so that three 2048-row stages fit in shared memory and the ring overlaps load, transform
     // and store (an 8-column tile leaves room for one stage only)
     static constexpr int kWidth = ospr_col_width(N);
-    static constexpr int kGroups = N >= 2048 ? 2 : 1;   // two consumer groups per CTA (ColPipeG2)
+    static constexpr int kGroups = N == 2048 ? 2 : 1;   // two consumer groups per CTA (ColPipeG2); 4096: one
+                                                        // 256-thread group on a single 133 KB stage
     struct Args {
         const float2 *tw;
         float2 *buf;
@@ -711,6 +796,58 @@ ospr_rows_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf
     }
 }
 
+// Pass C for N = 4096 (R-26): a two-warp group per row y, the chunk's pair rows read straight
+// from the pair buffer (coalesced), row FFT, |X|^2 summed over the pairs in registers, one
+// read-modify-write of the accumulator row.  The first nbt CTAs transpose the frame's sign
+// bytes (last chunk), as in ospr_rows_c_kernel; the finalize kernel symmetrises.
+template <int N>
+__global__ void __launch_bounds__(Row2W<N>::THREADS, 1)
+ospr_rows2w_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ buf, int npairs,
+                     float *__restrict__ acc, int accumulate, unsigned *ticket, int nbt, const uint8_t *__restrict__ bt,
+                     uint8_t *__restrict__ bits)
+{
+    HOLO_PDL_ENTRY();
+    if ((int)blockIdx.x < nbt) {
+        const int j = (int)blockIdx.x;
+        bits_transpose_block<N, Row2W<N>::THREADS>(bt, bits, j / BitsT<N>::BLOCKS_PER_Q, j % BitsT<N>::BLOCKS_PER_Q);
+        return;
+    }
+    if (ticket != nullptr && blockIdx.x == nbt && threadIdx.x == 0)
+        *ticket = 0u;                    // the finalize ticket, reset ahead of the finalize kernel
+    using P = fft::Plan<N>;
+    constexpr int R1 = P::R1, E = P::E;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const Row2WThread rt = row2w_thread();
+    float2 *sm = reinterpret_cast<float2 *>(smem_raw) + (size_t)rt.grp * P::SMEM;
+    const int cta = (int)blockIdx.x - nbt, nctas = (int)gridDim.x - nbt;
+    #pragma unroll 1
+    for (int y = cta * 2 + rt.grp; y < N; y += nctas * 2) {
+        float a[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            a[r] = 0.0f;
+        #pragma unroll 1
+        for (int p = 0; p < npairs; ++p) {
+            const float2 *src = buf + ((size_t)p * N + y) * N + rt.t;
+            float2 v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m] = src[R1 * m];
+            row2w_fft<N>(v, sm, tw, rt);
+#pragma unroll
+            for (int r = 0; r < E; ++r)
+                a[r] = __fmaf_rn(v[r].x, v[r].x, __fmaf_rn(v[r].y, v[r].y, a[r]));
+        }
+        constexpr float inv_p = 1.0f / ((float)N * (float)N);   // exact power of two
+        float *o = acc + (size_t)y * N + rt.t;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const float val = a[r] * inv_p;
+            o[R1 * r] = accumulate ? o[R1 * r] + val : val;
+        }
+    }
+}
+
 // ---- finalize + MSE -----------------------------------------------------------------------
 __device__ __forceinline__ void block_reduce_store(double (&s)[5], int nvals, double *dst)
 {
@@ -945,8 +1082,10 @@ ospr_finalize_kernel(const float *__restrict__ acc, const float *__restrict__ T,
     HOLO_PDL_ENTRY();
     constexpr int P = N * N, LOG = fft::ilog2(N), FB = FinPlan<N>::FB, ITER = FinPlan<N>::ITER;
     double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    // a fixed number of pixels per thread, fully unrolled: every load is in flight at once
-#pragma unroll
+    // a fixed number of pixels per thread, fully unrolled (N <= 2048: every load in flight at
+    // once; N = 4096, ITER = 111: unrolled by 8)
+    constexpr int UNR = ITER <= 32 ? ITER : 8;
+#pragma unroll UNR
     for (int i = 0; i < ITER; ++i) {
         const int k = (int)blockIdx.x * kFinThreads + (int)threadIdx.x + i * FB * kFinThreads;
         if (k >= P)
@@ -1147,7 +1286,18 @@ template <int N, bool ZOUT>
 static holo_status launch_pass_a(const float2 *tw, const float *Tf, const PhaseSrc &ps, int src, uint64_t sf_first,
                                  int np, int last_has_b, float2 *buf, cudaStream_t s, unsigned *zc = nullptr)
 {
-    if constexpr (N >= 1024) {
+    if constexpr (fft::Plan<N>::T > 32) {   // N = 4096: two warps per row
+        using RA = RowA4<N>;
+        auto kern = src == SRC_PRNG          ? ospr_rows_a4_kernel<N, LUT_PRNG, ZOUT>
+                  : src == SRC_TABLE         ? ospr_rows_a4_kernel<N, LUT_PRNG_TABLE, ZOUT>
+                  : ps.ix.mode == LUT_WRAP ? ospr_rows_a4_kernel<N, LUT_WRAP, ZOUT>
+                  : ps.ix.mode == LUT_POW2 ? ospr_rows_a4_kernel<N, LUT_POW2, ZOUT>
+                                           : ospr_rows_a4_kernel<N, LUT_GENERAL, ZOUT>;
+        (void)zc;
+        const int grid = pipe_grid(kern, RA::THREADS, RA::SMEM, np * RA::UNITS_PER_PAIR, 1);
+        return launch(ZOUT ? K_RANDOMISE : K_OSPR_ROWS_A, kern, dim3(grid), dim3(RA::THREADS), RA::SMEM, s, tw, Tf, ps,
+                      sf_first, np, last_has_b, buf);
+    } else if constexpr (N >= 1024) {
         using RA2 = RowA2<N>;
         auto kern = src == SRC_PRNG          ? ospr_rows_a2_kernel<N, LUT_PRNG, ZOUT>
                   : src == SRC_TABLE         ? ospr_rows_a2_kernel<N, LUT_PRNG_TABLE, ZOUT>
@@ -1205,7 +1355,8 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
     PhaseSrc ps;
     HOLO_TRY(make_phase_src(N, lut, n_lut, src, seed, phase_offset, &ps));
     // a7 fused into the last chunk's pass C when one warp owns a row (N >= 1024); else its own kernel
-    constexpr bool kFuse = RowC<N>::GPW == 1;
+    constexpr bool kWide = fft::Plan<N>::T > 32;   // N = 4096: two-warp rows (R-26)
+    constexpr bool kFuse = !kWide && RowC<N>::GPW == 1;
     const float scale = full ? 0.5f / (float)n_sub : 0.5f;
     for (int f = 0; f < n_frames; ++f) {
         const float *Tf = target + (size_t)f * P;
@@ -1239,7 +1390,14 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
                                 holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr));
                 }
             }
-            if (!fused) {
+            if constexpr (kWide) {
+                using R = Row2W<N>;
+                const int nbt = (last && holo_bits) ? nsh * BitsT<N>::BLOCKS_PER_Q : 0;
+                const int grid = pipe_grid(ospr_rows2w_c_kernel<N>, R::THREADS, R::SMEM, N / 2, 1);
+                HOLO_TRY(launch(K_OSPR_ROWS_C, ospr_rows2w_c_kernel<N>, dim3(nbt + grid), dim3(R::THREADS), R::SMEM, s,
+                                tw, (const float2 *)w.buf, np, w.acc, c0 > 0 ? 1 : 0, finalize_ticket(w.parts), nbt,
+                                (const uint8_t *)w.bt, holo_bits ? holo_bits + (size_t)f * nsh * (P / 8) : nullptr));
+            } else if (!fused) {
                 using RC = RowC<N>;
                 const int nbt = (last && holo_bits) ? nsh * BitsT<N>::BLOCKS_PER_Q : 0;
                 const int grid = pipe_grid(ospr_rows_c_kernel<N>, 64, RC::SMEM, RC::NGRP, 1);
@@ -1257,8 +1415,8 @@ static holo_status ospr_run(const float2 *tw, const float *target, int n_frames,
 
 holo_status check_n(int n)
 {
-    if (n < 16 || n > 2048 || (n & (n - 1)) != 0)
-        return set_error(HOLO_ERR_INVALID_ARG, "n must be a power of two in [16, 2048], got %d", n);
+    if (n < 16 || n > 4096 || (n & (n - 1)) != 0)
+        return set_error(HOLO_ERR_INVALID_ARG, "n must be a power of two in [16, 4096], got %d", n);
     return HOLO_OK;
 }
 
@@ -1330,6 +1488,7 @@ static holo_status ospr_entry(const float *target, int32_t n, int32_t n_frames, 
         HOLO_OSPR_CASE(512)
         HOLO_OSPR_CASE(1024)
         HOLO_OSPR_CASE(2048)
+        HOLO_OSPR_CASE(4096)
     default:
         return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }
@@ -1403,6 +1562,7 @@ extern "C" holo_status holo_debug_ospr_pairs(const float *target, int32_t n, int
         HOLO_PAIRS_CASE(512)
         HOLO_PAIRS_CASE(1024)
         HOLO_PAIRS_CASE(2048)
+        HOLO_PAIRS_CASE(4096)
     default:
         return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
     }
@@ -1485,6 +1645,7 @@ extern "C" holo_status holo_ospr_finalize(const float *target, const float *inte
             HOLO_FIN_CASE(512)
             HOLO_FIN_CASE(1024)
             HOLO_FIN_CASE(2048)
+            HOLO_FIN_CASE(4096)
         default:
             return set_error(HOLO_ERR_UNSUPPORTED, "n = %d", n);
         }

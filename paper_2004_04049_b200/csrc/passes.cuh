@@ -185,7 +185,8 @@ struct ColPipe {
 // its store has been read out, PREFETCH tiles ahead.
 template <int N, class Body, int NSTAGES>
 __global__ void __launch_bounds__(ColPipe<N, NSTAGES, Body::kWidth>::THREADS,
-                                  ((ColPipe<N, NSTAGES, Body::kWidth>::STAGES == 1 && N <= 1024) || Body::kWidth < 8) ? 2 : 1)
+                                  (N <= 2048 && ((ColPipe<N, NSTAGES, Body::kWidth>::STAGES == 1 && N <= 1024) ||
+                                                 Body::kWidth < 8)) ? 2 : 1)
 col_pipe_kernel(const __grid_constant__ CUtensorMap tmap, int ntiles, const typename Body::Args a, int rev)
 {
     HOLO_PDL_ENTRY();

@@ -193,7 +193,7 @@ holo_status twiddles(const float2 **pool)
         return HOLO_OK;
     }
     std::vector<float2> host(kTwPool, make_float2(0.f, 0.f));
-    for (int lg = 4; lg <= 11; ++lg) {
+    for (int lg = 4; lg <= 12; ++lg) {
         int n = 1 << lg, r1 = 1 << (lg / 2), r2 = n / r1, off = n - 16;
         for (int r = 0; r < r2; ++r)
             for (int t = 0; t < r1; ++t) {

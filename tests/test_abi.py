@@ -65,7 +65,8 @@ def test_ospr_arg_errors(L):
                                     FAKE, None, a["om"], a["ws"], a["wsb"], None)
 
     assert call(n=100) == _lib.HOLO_ERR_INVALID_ARG
-    assert call(n=4096) == _lib.HOLO_ERR_INVALID_ARG
+    assert call(n=8192) == _lib.HOLO_ERR_INVALID_ARG
+    assert call(n=8) == _lib.HOLO_ERR_INVALID_ARG
     assert call(S=0) == _lib.HOLO_ERR_INVALID_ARG
     assert call(b=3, e=3) == _lib.HOLO_ERR_INVALID_ARG
     assert call(e=9) == _lib.HOLO_ERR_INVALID_ARG

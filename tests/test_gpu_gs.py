@@ -193,11 +193,12 @@ def test_gs_groups_bit_identical(monkeypatch):
     assert torch.equal(a.mse, b.mse) and torch.equal(a.holo, b.holo) and torch.equal(a.intensity, b.intensity)
 
 
-@pytest.mark.parametrize("n", [512, 2048])
+@pytest.mark.parametrize("n", [512, 2048, 4096])
 def test_gs_large_sizes_one_iteration(n):
     """GS at the sizes the fixed configurations skip (512: two-pass rows with E = 16 values;
-    2048: the single-stage column pipeline and E = 64): first-iteration MSE and E_1 against
-    the oracle, continuous and 8-level constraints."""
+    2048: the single-stage column pipeline and E = 64; 4096: two-warp row passes and
+    4-column tiles, R-26): first-iteration MSE and E_1 against the oracle, continuous and
+    8-level constraints."""
     T = blobs_target(4242 + n, n, 8, n / 32, n / 8, Region.full(n))
     lg, lo = lut_pair(LUT_SEED, 4099)
     for Q in (0, 8):

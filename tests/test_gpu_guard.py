@@ -75,7 +75,7 @@ def _ospr_once(T, S, lut, sf, bits_fill, ws_fill=0x5A, prng=False):
 @pytest.mark.parametrize("n,F,S,L,sf,chunk_pairs", [
     (64, 2, 5, 1021, None, None), (64, 1, 5, 0, (1, 4), None), (256, 2, 4, 4096, None, 1),
     (256, 1, 7, 257, (2, 7), None), (1024, 1, 5, 1 << 16, None, 2), (1024, 1, 3, 1021, (0, 2), None),
-    (2048, 1, 3, 10007, None, None), (2048, 1, 4, 1 << 16, (2, 4), None)])
+    (2048, 1, 3, 10007, None, None), (2048, 1, 4, 1 << 16, (2, 4), None), (4096, 1, 3, 10007, None, None)])
 def test_ospr_outputs_guarded_and_complete(n, F, S, L, sf, chunk_pairs, monkeypatch):
     if chunk_pairs:
         monkeypatch.setenv("HOLO_OSPR_CHUNK_BYTES", str(chunk_pairs * n * n * 8))
@@ -119,7 +119,7 @@ def test_finalize_paths_guarded(n):
         assert torch.isfinite(g.t).all()
 
 
-@pytest.mark.parametrize("n,B,levels", [(64, 3, 0), (256, 2, 16), (1024, 2, 0), (2048, 1, 8)])
+@pytest.mark.parametrize("n,B,levels", [(64, 3, 0), (256, 2, 16), (1024, 2, 0), (2048, 1, 8), (4096, 1, 8)])
 def test_gs_outputs_guarded_and_complete(n, B, levels):
     T = torch.from_numpy(np.stack([blobs_target(30 + b, n, 6, n / 16, n / 6, Region.full(n))
                                    for b in range(B)])).cuda()
@@ -146,7 +146,7 @@ def test_gs_outputs_guarded_and_complete(n, B, levels):
     assert torch.equal(res[0][1], res[1][1])
 
 
-@pytest.mark.parametrize("n", [16, 128, 1024, 2048])
+@pytest.mark.parametrize("n", [16, 128, 1024, 2048, 4096])
 def test_fft2_and_lut_guarded(n):
     x = torch.randn(2, n, n, dtype=torch.complex64, device="cuda")
     for inv in (False, True):

@@ -64,6 +64,8 @@ def _mirror(R):
     (1024, 3, 65536, 0, (0, 3)),           # the C3 pool (rows_a2 kernel)
     (1024, 2, 1009, 12345, (0, 2)),        # rows_a2, LUT_GENERAL
     (2048, 1, 7, 3, (0, 1)),               # rows_a2, tiny LUT, unpaired
+    (4096, 3, 10007, 5, (0, 3)),           # rows_a4 (two warps per row, R-26), unpaired tail
+    (4096, 2, 1 << 16, 0, (0, 2)),         # rows_a4, LUT_POW2
 ])
 def test_pass_a_pairs_match_oracle(n, S, L, offset, rng):
     """The randomisation pass A feeds the row IFFT: conj(Z) with Z = H_a + i H_b,
@@ -82,7 +84,7 @@ def test_pass_a_pairs_match_oracle(n, S, L, offset, rng):
         assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, s)
 
 
-@pytest.mark.parametrize("n,offset", [(64, 0), (1024, (1 << 35) + 17)])
+@pytest.mark.parametrize("n,offset", [(64, 0), (1024, (1 << 35) + 17), (4096, 3)])
 def test_pass_a_pairs_prng_match_oracle(n, offset):
     """The same with the on-the-fly source (R-5 phases of SplitMix64 draws; recipe
     computed in fp64 on both sides, so R matches apply_phase_prng to fp32 rounding)."""
@@ -146,7 +148,7 @@ def test_ospr_prng_table_against_oracle(n, S, q):
 
 # ---- unitary DFT hook ------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 @pytest.mark.parametrize("inverse", [False, True])
 def test_fft2_matches_oracle(n, inverse):
     rng = np.random.default_rng(n)
@@ -371,6 +373,28 @@ def test_ospr_2048_prime_lut_all_subframes():
     against the oracle (P-3), the intensity conditionally (P-4) and the MSE (P-5)."""
     n, S, L, off = 2048, 3, 10007, 987654321
     T = blobs_target(11, n, 16, n / 16, n / 6.4, Region.upper_half(n))
+    lg, lo = lut_pair(LUT_SEED, L)
+    om = Region.upper_half(n).as_tuple()
+    res = hb.ospr_generate(cuda_target(T), S, lg, phase_offset=off, omega=om)
+    bits, I = to_np(res.bits)[0], to_np(res.intensity)[0]
+    for s in range(S):
+        _, h_re, _ = oracle.ospr_subframe(T, lo, off + s * n * n, want_h=True, want_intensity=False)
+        check_bits(bits[s], h_re, n)
+    check_intensity(I, oracle.replay_from_bits(bits, n))
+    _, _, mse_ref = oracle.ospr(T[None], S, lo, off, om)
+    assert rel(to_np(res.mse)[0], mse_ref[0]) <= REL_TOL
+
+
+@pytest.mark.parametrize("S,L,off,chunk_pairs", [(3, 10007, 987654321, 0), (4, 1 << 16, 0, 1)])
+def test_ospr_4096_all_subframes(S, L, off, chunk_pairs, monkeypatch):
+    """N = 4096, the top of the supported range (R-26: two-warp row passes, single-stage
+    4-column tiles): every sub-frame's bits against the oracle (P-3), the intensity
+    conditionally (P-4) and the MSE (P-5); a prime LUT with an unpaired tail, and a
+    power-of-two LUT run one pair per chunk (accumulation across chunks)."""
+    if chunk_pairs:
+        monkeypatch.setenv("HOLO_OSPR_CHUNK_BYTES", str(chunk_pairs * 4096 * 4096 * 8))
+    n = 4096
+    T = blobs_target(12, n, 16, n / 16, n / 6.4, Region.upper_half(n))
     lg, lo = lut_pair(LUT_SEED, L)
     om = Region.upper_half(n).as_tuple()
     res = hb.ospr_generate(cuda_target(T), S, lg, phase_offset=off, omega=om)
