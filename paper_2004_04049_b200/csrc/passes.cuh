@@ -2,7 +2,8 @@
 // is built from:
 //
 //  * row passes: each row transform is owned by the T = R1 threads of one warp
-//    (N <= 2048, so T <= 32) and synchronises with __syncwarp() only; warps run
+//    (N <= 2048, so T <= 32; N = 4096 has its own two-warp row kernels, rows2w.cuh)
+//    and synchronises with __syncwarp() only; warps run
 //    independently; rows arrive by 1D TMA (cp.async.bulk) into per-warp slots or are
 //    built in place (OSPR pass A), results go straight back (coalesced: lane t holds
 //    x = t + R1*m).
