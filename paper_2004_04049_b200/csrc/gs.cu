@@ -94,7 +94,9 @@ __device__ __forceinline__ GsAmp gs_amp(float m2, float tt, bool nz)
 }
 
 // ---- g0: R_0 = T * lut[(base_b + p) mod L] (or a given R_in) -> state; T sums over Omega -----------
-constexpr int kGsTBlocks = 64;   // CTAs per frame of the prepare kernel (fixed => deterministic sums)
+// CTAs per frame of the prepare kernel (fixed => deterministic sums; 256 keep small batches at
+// HBM speed: 4 frames of 4096^2 took 600 us with 64)
+constexpr int kGsTBlocks = 256;
 
 __device__ __forceinline__ uint32_t gs_lut_mod(uint32_t a, const LutIndexer &ix)
 {
@@ -188,7 +190,8 @@ gs_mse_kernel(const GsMetrics gm)
 template <int N, bool QUANT>
 struct GsColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
-    // columns per tile (4 measured 6 % slower for this body; N = 4096: 4, one 133 KB stage)
+    // columns per tile (4 measured 6 % slower for this body); N = 4096: 4, one 133 KB stage
+    // (2-column tiles on three stages, two groups: 26 % slower, half-sector row segments)
     static constexpr int kWidth = N >= 4096 ? 4 : 8;
     static constexpr int kGroups = 1;
     static constexpr bool kPrologue = true;

@@ -420,7 +420,7 @@ struct RowA4 {
 };
 
 template <int N, int LMODE, bool ZOUT = false>
-__global__ void __launch_bounds__(RowA4<N>::THREADS, 1)
+__global__ void __launch_bounds__(RowA4<N>::THREADS, 3)
 ospr_rows_a4_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const PhaseSrc ps, uint64_t sf_first,
                     int npairs, int last_pair_has_b, float2 *__restrict__ buf)
 {
@@ -509,10 +509,11 @@ struct OsprColBody {
     static constexpr int kStages = 3;   // measured best column-pipeline variant for this body
     // columns per tile: 8 (one packed byte per tile row); N = 2048: 4 (a nibble per tile row),
     // so that three 2048-row stages fit in shared memory and the ring overlaps load, transform
-    // and store (an 8-column tile leaves room for one stage only)
+    // and store (an 8-column tile leaves room for one stage only).  N = 4096: one 4-column stage
+    // of 133 KB and one 256-thread group (2-column tiles with three stages measured 27 % slower:
+    // 16-byte row segments halve the DRAM sector efficiency)
     static constexpr int kWidth = ospr_col_width(N);
-    static constexpr int kGroups = N == 2048 ? 2 : 1;   // two consumer groups per CTA (ColPipeG2); 4096: one
-                                                        // 256-thread group on a single 133 KB stage
+    static constexpr int kGroups = N == 2048 ? 2 : 1;   // two consumer groups per CTA (ColPipeG2)
     struct Args {
         const float2 *tw;
         float2 *buf;
