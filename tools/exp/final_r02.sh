@@ -25,4 +25,15 @@ python tools/prof_run.py gs64 1 > "$out/gs_plain.log" 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:col_pipe|gs_rows_kernel" -s 2 -c 2 \
     -o "$out/gs64" python tools/prof_run.py gs64 1 > "$out/ncu_gs.log" 2>&1
 echo "ncu gs rc=$?"
+# summaries on the box (the .ncu-rep files exceed what gpurun copies back), then drop the reports
+for r in ospr c5 gs64; do
+    [ -f "$out/$r.ncu-rep" ] || continue
+    python tools/ncu_summary.py "$out/$r.ncu-rep" --src 12 > "$out/ncu_${r}_summary.txt" 2>&1
+    ncu -i "$out/$r.ncu-rep" --page raw --csv > "$out/ncu_${r}_raw.csv" 2>/dev/null
+done
+cp profiles/ncu_traffic.json "$out/ncu_traffic_before.json"
+[ -f "$out/ospr.ncu-rep" ] && python tools/ncu_traffic.py "$out/ospr.ncu-rep" "ncu --set full --clock-control none (caches flushed per replay); OSPR classes: tools/prof_run.py ospr 3 (C3 OSPR call, 12 pairs, L=2^16), capture ${1:-r02_final}/ospr" > /dev/null
+[ -f "$out/gs64.ncu-rep" ] && python tools/ncu_traffic.py "$out/gs64.ncu-rep" "gs_cols/gs_rows: tools/prof_run.py gs64 1 (the whole C4 launch group: 64 frames, 512 MiB state streaming from HBM), capture ${1:-r02_final}/gs64" --merge > /dev/null
+cp profiles/ncu_traffic.json "$out/ncu_traffic.json"
+rm -f "$out"/*.ncu-rep
 ls -la "$out"
