@@ -44,6 +44,9 @@ def main():
         out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda'],
                              capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(out)))
+        # the page may start with per-file banner rows ("File Name", path) before the header
+        while rows and not any(c.startswith('Warp Stall Sampling') for c in rows[0]):
+            rows = rows[1:]
         if not rows:
             return
         hh = rows[0]
