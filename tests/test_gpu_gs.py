@@ -197,11 +197,15 @@ def test_gs_groups_bit_identical(monkeypatch):
 def test_gs_large_sizes_one_iteration(n):
     """GS at the sizes the fixed configurations skip (512: two-pass rows with E = 16 values;
     2048: the single-stage column pipeline and E = 64; 4096: two-warp row passes and
-    4-column tiles, R-26): first-iteration MSE and E_1 against the oracle, continuous and
-    8-level constraints."""
+    4-column tiles, R-26): MSE and E_k against the oracle, continuous (three iterations, so
+    iterations 1 and 2 go through the column pass's prologue reduction of the previous row
+    pass's partials) and 8-level (first iteration: later ones may take fp32-vs-fp64 level
+    decisions differently, R-22) constraints."""
     T = blobs_target(4242 + n, n, 8, n / 32, n / 8, Region.full(n))
     lg, lo = lut_pair(LUT_SEED, 4099)
-    for Q in (0, 8):
-        res = hb.gs_generate(cuda_target(T[None]), 1, lg, phase_offset=77, levels=Q)
-        ref = oracle.gs(T, 1, lo, 77, Q, (0, n, 0, n))
-        assert rel(to_np(res.mse)[0, 0], ref["mse"][0]) <= REL_TOL, (n, Q)
+    for Q, iters in ((0, 3), (8, 1)):
+        res = hb.gs_generate(cuda_target(T[None]), iters, lg, phase_offset=77, levels=Q)
+        ref = oracle.gs(T, iters, lo, 77, Q, (0, n, 0, n))
+        for k in range(iters):
+            assert rel(to_np(res.mse)[0, k], ref["mse"][k]) <= REL_TOL, (n, Q, k)
+            assert rel(to_np(res.err_e)[0, k], ref["E"][k]) <= REL_TOL, (n, Q, k)
