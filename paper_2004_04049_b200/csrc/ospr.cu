@@ -448,14 +448,32 @@ ospr_rows_a4_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
             const Base a1 = PR::row(ps, ba, y), a2 = PR::row(ps, ba, ym);
             const Base b1 = PR::row(ps, bb, y), b2 = PR::row(ps, bb, ym);
             const float *T1 = T + (size_t)y * N, *T2 = T + (size_t)ym * N;
+            bool fast = false;
+            if constexpr (LMODE == LUT_WRAP) {
+                const uint32_t lim = ps.ix.L - (uint32_t)N;
+                fast = a1 <= lim && a2 <= lim && b1 <= lim && b2 <= lim;
+            }
+            if (fast) {   // no LUT row wraps: plain offsets from the row bases
+                const float2 *LA1 = ps.lut + (uint32_t)a1, *LA2 = ps.lut + (uint32_t)a2;
+                const float2 *LB1 = ps.lut + (uint32_t)b1, *LB2 = ps.lut + (uint32_t)b2;
+#pragma unroll 8
+                for (int x = tid; x < N; x += RA::THREADS) {
+                    const int xm = (N - x) & (N - 1);
+                    const float t1 = T1[x], t2 = T2[xm];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, LA1[x], LA2[xm], LB1[x], LB2[xm]);
+                    s0[x] = z.z1;
+                    s1[xm] = z.z2;
+                }
+            } else {
 #pragma unroll 4
-            for (int x = tid; x < N; x += RA::THREADS) {
-                const int xm = (N - x) & (N - 1);
-                const float t1 = T1[x], t2 = T2[xm];
-                const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a2, xm),
-                                       PR::at(ps, b1, x), PR::at(ps, b2, xm));
-                s0[x] = z.z1;
-                s1[xm] = z.z2;
+                for (int x = tid; x < N; x += RA::THREADS) {
+                    const int xm = (N - x) & (N - 1);
+                    const float t1 = T1[x], t2 = T2[xm];
+                    const ZPair z = z_pair(t1, t2, t1 * bsc, t2 * bsc, PR::at(ps, a1, x), PR::at(ps, a2, xm),
+                                           PR::at(ps, b1, x), PR::at(ps, b2, xm));
+                    s0[x] = z.z1;
+                    s1[xm] = z.z2;
+                }
             }
         } else {       // unit 0: rows 0 and N/2, each its own mirror; group grp builds row grp
             const int yy = grp ? N / 2 : 0;
@@ -829,6 +847,14 @@ ospr_rows2w_c_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ b
             a[r] = 0.0f;
         #pragma unroll 1
         for (int p = 0; p < npairs; ++p) {
+            if (rt.t == 0) {   // the group's next pair row into L2 while this one transforms
+                const int yn = y + nctas * 2;
+                const float2 *nx = p + 1 < npairs ? buf + ((size_t)(p + 1) * N + y) * N
+                                 : yn < N         ? buf + (size_t)yn * N
+                                                  : nullptr;
+                if (nx != nullptr)
+                    tma::prefetch_l2(nx, (uint32_t)N * 8);
+            }
             const float2 *src = buf + ((size_t)p * N + y) * N + rt.t;
             float2 v[E];
 #pragma unroll
