@@ -21,6 +21,15 @@
 
 #include <type_traits>
 
+// HOLO_L2PF: the fused OSPR pass C at N <= 1024 also prefetches each warp's pair row after the
+// next one into L2 (cp.async.bulk.prefetch), so that its TMA load finds it there: 33.7 -> 32.5 us
+// at C3 (prefetch distance HOLO_CF_PFD, ospr.cu).  Measured and not kept: the same at N = 2048 (C5 0.617 -> 0.622 ms), in the GS row pass
+// (no gain), and for the column pipelines' 2D tiles (cp.async.bulk.prefetch.tensor: OSPR 48.6 ->
+// 50.2 us, GS 228 -> 262 us, C5 0.618 -> 0.89 ms).
+#ifndef HOLO_L2PF
+#define HOLO_L2PF 1
+#endif
+
 namespace holo {
 
 // A column-pipeline body may declare `static constexpr bool kPrologue = true` and a
