@@ -988,6 +988,10 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
             tma::mbar_arrive_expect_tx(&bar[i], RC::IN_BYTES);
             tma::load_1d(slot(i), src(p0 + i), RC::IN_BYTES, &bar[i]);
         }
+#ifndef HOLO_CF_PFD
+#define HOLO_CF_PFD 2   // measured at C3: 1 -> 110.6, 2 -> 110.5, 3 -> 110.8, none -> 111.3 us per step
+#endif
+    // (prefetching the rows before the loop's first prefetch as well, at CTA start: 33.6 vs 32.3 us)
     float a[E];
 #pragma unroll
     for (int r = 0; r < E; ++r)
@@ -995,9 +999,6 @@ ospr_rows_cf_kernel(const float2 *__restrict__ tw, const float2 *__restrict__ bu
     uint32_t k = 0;
     #pragma unroll 1
     for (int p = p0; p < p1; ++p, ++k) {
-#ifndef HOLO_CF_PFD
-#define HOLO_CF_PFD 2   // measured at C3: 1 -> 110.6, 2 -> 110.5, 3 -> 110.8, none -> 111.3 us per step
-#endif
         if (HOLO_L2PF && N <= 1024 && lane == 0 && p + NS + HOLO_CF_PFD - 1 < p1 - 1)   // a later pair row into L2
             tma::prefetch_l2(src(p + NS + HOLO_CF_PFD), RC::IN_BYTES);
         const int si = NS > 1 ? (int)(k % NS) : 0;
