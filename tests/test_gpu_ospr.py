@@ -84,7 +84,7 @@ def test_pass_a_pairs_match_oracle(n, S, L, offset, rng):
         assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, s)
 
 
-@pytest.mark.parametrize("n,offset", [(64, 0), (1024, (1 << 35) + 17), (4096, 3)])
+@pytest.mark.parametrize("n,offset", [(64, 0), (1024, (1 << 35) + 17), (2048, 11), (4096, 3)])
 def test_pass_a_pairs_prng_match_oracle(n, offset):
     """The same with the on-the-fly source (R-5 phases of SplitMix64 draws; recipe
     computed in fp64 on both sides, so R matches apply_phase_prng to fp32 rounding)."""
@@ -111,7 +111,7 @@ def test_phase_table_matches_recipe(q):
     assert np.array_equal(tbl.imag.view(np.uint32), ref[:, 1].view(np.uint32))
 
 
-@pytest.mark.parametrize("n,q,offset", [(64, 8, 0), (64, 2, 977), (256, 12, 3 << 33), (1024, 16, 5)])
+@pytest.mark.parametrize("n,q,offset", [(64, 8, 0), (64, 2, 977), (256, 12, 3 << 33), (1024, 16, 5), (2048, 8, 7)])
 def test_pass_a_pairs_prng_table_match_oracle(n, q, offset):
     """P:170 / R-25: pass A with the PRNG + 2^q sin/cos table source equals the oracle's
     quantised source (apply_phase_prng_q) to fp32 rounding."""
@@ -448,7 +448,8 @@ def test_ospr_graph_replay_bit_identical():
     assert torch.equal(out.mse, eager.mse)
 
 
-@pytest.mark.parametrize("n,S,offset", [(64, 8, 0), (128, 5, 12345), (256, 6, (1 << 33) + 7)])
+@pytest.mark.parametrize("n,S,offset", [(64, 8, 0), (128, 5, 12345), (256, 6, (1 << 33) + 7), (2048, 3, 5),
+                                        (4096, 3, 0)])
 def test_ospr_prng_source_equals_full_length_lut(n, S, offset):
     """phases drawn on the fly (SplitMix64 + R-5 in pass A) give
     bit-identical holograms, intensity and MSE to a pool from the same seed that is longer
