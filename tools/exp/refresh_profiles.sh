@@ -8,3 +8,4 @@ cp "$d/ncu_ospr_summary.txt" profiles/r02_ncu_ospr_c3.txt
 cp "$d/ncu_c5_summary.txt" profiles/r02_ncu_ospr_c5.txt
 cp "$d/ncu_gs64_summary.txt" profiles/r02_ncu_gs_c4_64frames.txt
 cp "$d/ncu_traffic.json" profiles/ncu_traffic.json
+cp "$d/launches_warm.csv" profiles/r02_launches_warm.csv
