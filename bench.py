@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--lut", type=int, default=1 << 16, help="headline LUT length")
     ap.add_argument("--ospr-shard", choices=["frames", "subframes"], default="frames",
                     help="N > 1: each rank its own C3 frame set (weak, no collective; default) or one frame "
-                         "set's sub-frames split across ranks + NCCL all-reduce of the intensity (strong)")
+                         "set's sub-frames split across ranks + NCCL reduce-scatter of the partial intensity, "
+                         "a7 on the owned rows and an all-reduce of five doubles (strong)")
     ap.add_argument("--no-gs", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
