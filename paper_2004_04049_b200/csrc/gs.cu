@@ -140,6 +140,87 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
     block_reduce_n(s, 2, tparts + ((size_t)fr * kGsTBlocks + blockIdx.x) * 2);
 }
 
+// g0 fused with the first row transform (N <= 2048): items are GPW-row groups, as in the row
+// pipeline; each warp builds conj(R_0) of its rows straight into registers (the same products
+// as gs_prepare_kernel), row-FFTs them (F{conj(R_0)}, as rows_fft_kernel) and writes the state
+// once, and stores its fp64 partial sums of T^2, T^4 over Omega per item (reduced per frame in a
+// fixed order by gs_tsum_kernel).  Saves the prepare kernel's state write and the row FFT's read.
+template <int N>
+__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+gs_init_rows_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut,
+                    LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t frame0,
+                    const float2 *__restrict__ r_in, holo_region om, float2 *__restrict__ state,
+                    double *__restrict__ tparts, int nitems)
+{
+    HOLO_PDL_ENTRY();
+    using P = fft::Plan<N>;
+    using RP = RowPipe<N>;
+    constexpr int R1 = P::R1, E = P::E, GPW = RP::GPW, NGRP = N / GPW;
+    constexpr uint32_t XB = (RP::XCH_BYTES + 127) / 128 * 128;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
+    float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * XB);
+    fft::Twiddles<N> twr;
+    twr.load(tw, t);
+    #pragma unroll 1
+    for (int item = blockIdx.x * RP::WPC + warp; item < nitems; item += gridDim.x * RP::WPC) {
+        const int fr = item / NGRP, grp = item % NGRP, y = grp * GPW + g;
+        const size_t rofs = ((size_t)fr * N + y) * N;
+        uint32_t base = 0;
+        if (lut != nullptr)
+            base = ix.mod64((uint64_t)off_mod + (uint64_t)ix.mod64(frame0 + fr) * (uint64_t)p_mod);
+        const bool row_in = y >= om.row0 && y < om.row1;
+        double s2 = 0.0, s4 = 0.0;
+        float2 v[E];
+        float tv[E];
+        // one branch per source around whole unrolled loops, so that every load of the row is in
+        // flight at once (per-element branches serialised the loads: 0.95 ms vs 0.19 ms at C4)
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            tv[m] = __ldg(T + rofs + t + R1 * m);
+        if (r_in != nullptr) {
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m] = conjf2(r_in[rofs + t + R1 * m]);
+        } else if (lut != nullptr) {
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m] = __ldg(lut + gs_lut_mod(base + (uint32_t)(y * N + t + R1 * m), ix));
+#pragma unroll
+            for (int m = 0; m < E; ++m)   // a2, exact fp32 products; the state is kept conjugated
+                v[m] = make_float2(__fmul_rn(tv[m], v[m].x), -__fmul_rn(tv[m], v[m].y));
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[m] = make_float2(tv[m], -0.0f);
+        }
+        if (row_in) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int x = t + R1 * m;
+                if (x >= om.col0 && x < om.col1) {
+                    const double td = tv[m], t2 = td * td;
+                    s2 += t2;
+                    s4 += t2 * t2;
+                }
+            }
+        }
+        fft::fft2pass<N, false, 1, true>(v, sl + g * P::SMEM, t, twr);   // F{conj(R_0)}
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            state[rofs + t + R1 * m] = v[m];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s2 += __shfl_down_sync(0xffffffffu, s2, o);
+            s4 += __shfl_down_sync(0xffffffffu, s4, o);
+        }
+        if (lane == 0) {
+            tparts[((size_t)fr * NGRP + grp) * 2] = s2;
+            tparts[((size_t)fr * NGRP + grp) * 2 + 1] = s4;
+        }
+    }
+}
+
 // g4 of iteration k for the frames of a launch group (pointers offset to the group).
 struct GsMetrics {
     const float *a0;      // [G] prior a0 = sum_Omega T^2 / |Omega| (gs_tsum_kernel)
@@ -521,13 +602,18 @@ gs_rows2w_kernel(const float2 *__restrict__ tw, float2 *state, const float *__re
 // One CTA per frame of a launch group: fixed-order sum of the prepare kernel's T partials ->
 // tsum[frame] = (sum T^2, sum T^4) over Omega and the prior a0 = sum T^2 / |Omega| that the
 // row pass takes its metric partials about (exactly R-12's a for the full plane, by Parseval).
-__global__ void __launch_bounds__(kGsTBlocks)
-gs_tsum_kernel(const double *__restrict__ tparts, double inv_count, double *__restrict__ tsum, float *__restrict__ a0)
+__global__ void __launch_bounds__(256)
+gs_tsum_kernel(const double *__restrict__ tparts, int nparts, double inv_count, double *__restrict__ tsum,
+               float *__restrict__ a0)
 {
     HOLO_PDL_ENTRY();
     const int fr = blockIdx.x;
-    const double *q = tparts + ((size_t)fr * kGsTBlocks + threadIdx.x) * 2;
-    double u[2] = {q[0], q[1]};
+    double u[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {   // fixed order
+        const double *q = tparts + ((size_t)fr * nparts + i) * 2;
+        u[0] += q[0];
+        u[1] += q[1];
+    }
     __shared__ double o[2];
     block_reduce_n(u, 2, o);
     __syncthreads();
@@ -576,7 +662,7 @@ struct GsWs {
     float2 *qtab;
     float2 *state;
     double *parts;    // [G][NBLK][kGsParts] row-pass item partials of the current iteration
-    double *tparts;   // [G][kGsTBlocks][2] prepare-kernel partials of sum T^2, T^4
+    double *tparts;   // [G][max(kGsTBlocks, N)][2] init partials of sum T^2, T^4 (per CTA or per row item)
     double *tsum;     // [G][2]
     float *a0;        // [G]
 };
@@ -593,7 +679,7 @@ static size_t gs_ws_layout(int n, int batch, char *base, GsWs *w)
     const size_t o_parts = off;
     off = al256(off + (size_t)G * nblk * kGsParts * sizeof(double));
     const size_t o_tparts = off;
-    off = al256(off + (size_t)G * kGsTBlocks * 2 * sizeof(double));
+    off = al256(off + (size_t)G * (n > kGsTBlocks ? n : kGsTBlocks) * 2 * sizeof(double));
     const size_t o_tsum = off;
     off = al256(off + (size_t)G * 2 * sizeof(double));
     const size_t o_a0 = off;
@@ -634,13 +720,25 @@ static holo_status gs_run(const float2 *tw, const float *target, int batch, int 
         HOLO_TRY(launch(K_GS_COLS, gs_qtab_kernel, dim3((levels + 255) / 256), dim3(256), 0, s, levels, w.qtab));
     for (int g0 = 0; g0 < batch; g0 += G) {
         const int ng = (batch - g0) < G ? (batch - g0) : G;
-        HOLO_TRY(launch(K_GS_ROWS_INIT, gs_prepare_kernel<N>, dim3(kGsTBlocks, ng), dim3(256), 0, s,
-                        target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
-                        r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state,
-                        w.tparts));
-        HOLO_TRY(launch(K_MSE_REDUCE, gs_tsum_kernel, dim3(ng), dim3(kGsTBlocks), 0, s, (const double *)w.tparts,
-                        inv_cnt, w.tsum, w.a0));
-        HOLO_TRY((launch_row_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));    // F{conj(R_0)}
+        if constexpr (!GsRowCfg<N>::kWide) {   // g0 fused with the first row FFT
+            using RP = RowPipe<N>;
+            constexpr size_t smem = (size_t)RP::WPC * ((RP::XCH_BYTES + 127) / 128 * 128);
+            const int nitems = ng * (N / RP::GPW);
+            const int grid = pipe_grid(gs_init_rows_kernel<N>, RP::WPC * 32, smem, nitems, RP::WPC);
+            HOLO_TRY(launch(K_GS_ROWS_INIT, gs_init_rows_kernel<N>, dim3(grid), dim3(RP::WPC * 32), smem, s, tw,
+                            target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
+                            r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state, w.tparts, nitems));
+            HOLO_TRY(launch(K_MSE_REDUCE, gs_tsum_kernel, dim3(ng), dim3(256), 0, s, (const double *)w.tparts,
+                            N / RP::GPW, inv_cnt, w.tsum, w.a0));
+        } else {
+            HOLO_TRY(launch(K_GS_ROWS_INIT, gs_prepare_kernel<N>, dim3(kGsTBlocks, ng), dim3(256), 0, s,
+                            target + g0 * P, lut, ix, off_mod, p_mod, (uint64_t)g0,
+                            r_in ? r_in + g0 * P : (const float2 *)nullptr, om, w.state,
+                            w.tparts));
+            HOLO_TRY(launch(K_MSE_REDUCE, gs_tsum_kernel, dim3(ng), dim3(256), 0, s, (const double *)w.tparts,
+                            kGsTBlocks, inv_cnt, w.tsum, w.a0));
+            HOLO_TRY((launch_row_fft<N, false>(K_GS_ROWS_INIT, tw, w.state, w.state, ng * N, s)));   // F{conj(R_0)}
+        }
         using RP = RowPipe<N>;
         const float *Tg = target + g0 * P;
         GsMetrics gm{w.a0, w.tsum, w.parts, mse ? mse + (size_t)g0 * iters : (double *)nullptr,
