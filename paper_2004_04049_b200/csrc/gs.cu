@@ -146,7 +146,7 @@ gs_prepare_kernel(const float *__restrict__ T, const float2 *__restrict__ lut, L
 // once, and stores its fp64 partial sums of T^2, T^4 over Omega per item (reduced per frame in a
 // fixed order by gs_tsum_kernel).  Saves the prepare kernel's state write and the row FFT's read.
 template <int N>
-__global__ void __launch_bounds__(RowPipe<N>::WPC * 32)
+__global__ void __launch_bounds__(RowPipe<N>::WPC * 32, N <= 1024 ? 4 : 1)
 gs_init_rows_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, const float2 *__restrict__ lut,
                     LutIndexer ix, uint32_t off_mod, uint32_t p_mod, uint64_t frame0,
                     const float2 *__restrict__ r_in, holo_region om, float2 *__restrict__ state,
@@ -160,7 +160,7 @@ gs_init_rows_kernel(const float2 *__restrict__ tw, const float *__restrict__ T, 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane / R1, t = lane % R1;
     float2 *sl = reinterpret_cast<float2 *>(smem_raw + (size_t)warp * XB);
-    fft::Twiddles<N> twr;
+    fft::Twiddles<N, false> twr;                         // pool twiddles: four CTAs per SM at N = 1024
     twr.load(tw, t);
     #pragma unroll 1
     for (int item = blockIdx.x * RP::WPC + warp; item < nitems; item += gridDim.x * RP::WPC) {
