@@ -514,7 +514,7 @@ def run_gpu(args):
         hosts = [torch.from_numpy(target_for(w3)).pin_memory() for _ in range(3)]
         lut_e2e = torch.empty(max(args.lut, 1), dtype=torch.complex64, device=dev)
         stream = hb.OsprStream(n, S, lut_e2e[:args.lut], depth=3, phase_offset=rank * S * P, frame_stride=world,
-                               before_each=lambda: hb.lut_generate(LUT_SEED, args.lut, out=lut_e2e[:args.lut]))
+                               lut_seed=LUT_SEED)                       # a0 per frame set, native sequencer
         for i in range(args.warmup):
             stream.submit(hosts[i % 3])
         stream.drain()
@@ -534,17 +534,34 @@ def run_gpu(args):
             reps.append(max_over_ranks(a.elapsed_time(b), world))
         tm = statistics.median(reps)
         mse_e2e = float(stream.result(stream.f - 1)[1][0])
+        # the box's own host-link rates for these transfers (copies alone, pinned buffers), so that
+        # the e2e number can be read against them: it is bounded by max(kernels, H2D, D2H) per set
+        pcie = {}
+        dev_t = torch.empty(hosts[0].shape, dtype=torch.float32, device=dev)
+        dev_b = torch.empty(stream.bits_host[0].shape, dtype=torch.uint8, device=dev)
+        for name, dst, src in (("h2d", dev_t, hosts[0]), ("d2h", stream.bits_host[0], dev_b)):
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                dst.copy_(src, non_blocking=True)
+            b.record()
+            torch.cuda.synchronize()
+            pcie[name + "_gbs"] = 20 * src.numel() * src.element_size() / (a.elapsed_time(b) * 1e-3) / 1e9
+        del dev_t, dev_b
         result["e2e"] = {"value": world * S * ke / (tm / 1e3), "unit": UNIT, "frame_sets_timed": ke,
                          "runs_ms": reps, "statistic": "median of 3 runs",
                          "h2d_bytes_per_step": world * hosts[0].numel() * 4,
                          "d2h_bytes_per_step": world * (stream.bits_host[0].numel() + 8),
                          "bytes_per_step": "all ranks (one frame set per rank per step)",
                          "ms_per_step": tm / ke, "frame_sets": [first, stream.f], "mse_last": mse_e2e,
+                         "host_link": pcie,
                          "what": "paper_2004_04049_b200.OsprStream (public API): per frame set a pinned host target "
                                  "-> device, a0 LUT build, ospr_generate (a1-a7) with the continuing cursor, packed "
                                  "holograms + MSE -> pinned host; H2D of f+1 and D2H of f-1 overlap the kernels of "
-                                 "f (3 CUDA streams, 3 slots, eager launches); timed by events from the first "
-                                 "H2D to the last D2H",
+                                 "f (3 CUDA streams, 3 slots, eager launches, one native holo_ospr_stream_submit "
+                                 "per frame set); timed by events from the first H2D to the last D2H",
                          "l2": "not flushed between pipelined frame sets; every input of a frame set is produced "
                                "inside it (target by its H2D, LUT by a0)"}
     elif not args.no_e2e:

@@ -294,6 +294,66 @@ holo_status holo_gs_step(const holo_c64 *r_in, const float *target, int32_t n, i
                          void *ws, size_t ws_bytes, holo_stream stream);
 
 /* ------------------------------------------------------------------------
+ * OSPR frame stream for a binary SLM (PAPER.md P:162:
+ * a 1024x1024 ferroelectric display shows the N_SF binary sub-frames of each
+ * video frame; P:72 / R-2: frame set f continues the phase cursor).
+ *
+ * A stream owns three non-blocking CUDA streams (h2d, comp, d2h) and per-slot
+ * events; everything else is the caller's.  holo_ospr_stream_submit enqueues
+ * frame set f in slot f mod depth: H2D of the target, [a0] +
+ * holo_ospr_generate (a1-a7) at cursor phase_offset + f * frame_stride *
+ * n_sub * n^2 (advance = 0: phase_offset for every f), D2H of the packed
+ * holograms, the MSE and optionally the intensity.  Consecutive frame sets'
+ * copies overlap each other's kernels; the host never blocks in submit.
+ * ------------------------------------------------------------------------ */
+
+typedef struct holo_ospr_stream holo_ospr_stream;   /* opaque */
+
+/* slots: depth * 7 pointers, per slot in this order:
+ *   t_dev      device float [n][n]            target of the slot's frame set
+ *   bits_dev   device uint8 [n_sub][n][n/8]    packed holograms (R-8)
+ *   inten_dev  device float [n][n]            mean replay intensity
+ *   mse_dev    device double [1]
+ *   bits_host  host (pinned) uint8 [n_sub][n][n/8]
+ *   mse_host   host (pinned) double [1]
+ *   inten_host host (pinned) float [n][n], or NULL (intensity not shipped)
+ * lut: device pool of n_lut entries (NULL iff n_lut == 0); regen_lut != 0
+ *   regenerates it (holo_lut_generate(lut_seed, n_lut), step a0) on the
+ *   compute stream before each frame set.  ws: holo_ospr_workspace_size(n, 1,
+ *   n_sub) bytes, used by one frame set at a time.  depth in [1, 16].
+ * All buffers must stay valid until holo_ospr_stream_destroy.  Errors:
+ *   INVALID_ARG (sizes, NULL buffers, region), WORKSPACE, CUDA. */
+holo_status holo_ospr_stream_create(int32_t n, int32_t n_sub, int32_t depth, const holo_c64 *lut,
+                                    uint64_t n_lut, int32_t regen_lut, uint64_t lut_seed,
+                                    uint64_t phase_offset, uint64_t frame_stride, int32_t advance,
+                                    holo_region omega, void *const *slots, void *ws, size_t ws_bytes,
+                                    holo_ospr_stream **out);
+
+/* Enqueue the next frame set from target_host (float [n][n]; pinned for an
+ * asynchronous copy; the caller keeps it unchanged until the frame set is
+ * done).  *frame (nullable) receives its index f.  Slot reuse waits on the
+ * device for the slot's previous frame set, never on the host. */
+holo_status holo_ospr_stream_submit(holo_ospr_stream *st, const float *target_host, int64_t *frame);
+
+/* Block until frame set `frame` (one of the last `depth` submitted) has its
+ * outputs in the slot's host buffers, valid until frame + depth is submitted. */
+holo_status holo_ospr_stream_wait(holo_ospr_stream *st, int64_t frame);
+
+/* 1 if frame set `frame`'s outputs are in host memory, 0 if pending, -1 if
+ * it is not among the last `depth` submitted (or on a CUDA error). */
+int32_t holo_ospr_stream_done(holo_ospr_stream *st, int64_t frame);
+
+/* Block until every submitted frame set is complete. */
+holo_status holo_ospr_stream_drain(holo_ospr_stream *st);
+
+/* The stream's three CUDA streams (h2d, comp, d2h), e.g. to record timing
+ * events or to order other work after a frame set; owned by the stream. */
+holo_status holo_ospr_stream_handles(holo_ospr_stream *st, holo_stream *h2d, holo_stream *comp, holo_stream *d2h);
+
+/* Drain and release the stream's CUDA streams and events (NULL: no-op). */
+void holo_ospr_stream_destroy(holo_ospr_stream *st);
+
+/* ------------------------------------------------------------------------
  * Instrumentation.
  * ------------------------------------------------------------------------ */
 

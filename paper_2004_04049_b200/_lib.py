@@ -62,6 +62,14 @@ SIGNATURES = {
     "holo_debug_randomise": (C.c_int, [_vp, _i32, _vp, _u64, _u64, _vp, _vp]),
     "holo_gs_step": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, HoloRegion, _vp, _sz,
                                _vp]),
+    "holo_ospr_stream_create": (C.c_int, [_i32, _i32, _i32, _vp, _u64, _i32, _u64, _u64, _u64, _i32, HoloRegion,
+                                          _vp, _vp, _sz, C.POINTER(_vp)]),
+    "holo_ospr_stream_submit": (C.c_int, [_vp, _vp, C.POINTER(C.c_int64)]),
+    "holo_ospr_stream_wait": (C.c_int, [_vp, C.c_int64]),
+    "holo_ospr_stream_done": (_i32, [_vp, C.c_int64]),
+    "holo_ospr_stream_drain": (C.c_int, [_vp]),
+    "holo_ospr_stream_destroy": (None, [_vp]),
+    "holo_ospr_stream_handles": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "holo_launch_count": (_u64, []),
     "holo_profile_enable": (C.c_int, [_i32]),
     "holo_profile_read": (C.c_int, [C.c_char_p, C.POINTER(_u64), C.POINTER(C.c_double)]),

@@ -23,7 +23,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v",
 ]
-TUS = ["runtime.cu", "lut.cu", "ospr.cu", "gs.cu", "hooks.cu"]
+TUS = ["runtime.cu", "lut.cu", "ospr.cu", "gs.cu", "hooks.cu", "stream.cu"]
 
 
 def sources():

@@ -13,11 +13,14 @@ overlap the steps of consecutive frame sets:
 
 with `depth` device slots for the per-frame buffers (targets and outputs) and one workspace (the
 compute steps of consecutive frame sets run in order on `comp`).  Cross-stream order comes from
-CUDA events only; the host never blocks in submit().  Every kernel is libholo's: this module is
-plumbing (PyTorch streams, events and pinned memory).
+CUDA events only; the host never blocks in submit().  The sequencing is native
+(holo_ospr_stream_*: one C call per frame set enqueues the copies, a0 when `lut_seed` is given,
+and the passes); this module allocates the buffers.  A Python `before_each` hook (any work to
+enqueue on the compute stream ahead of each frame set) selects an equivalent Python sequencer.
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Callable, Optional, Sequence, Tuple
 
 import torch
@@ -40,7 +43,7 @@ class OsprStream:
                  phase_offset: int = 0, advance: bool = True, frame_stride: int = 1,
                  omega: Optional[Sequence[int]] = None,
                  want_intensity: bool = False, before_each: Optional[Callable[[], None]] = None,
-                 device: Optional[torch.device] = None):
+                 lut_seed: Optional[int] = None, device: Optional[torch.device] = None):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -76,6 +79,31 @@ class OsprStream:
         self._args = [(t.data_ptr(), n, 1, n_sub, lp, L) for t in self.t_dev]
         self._tail = [(0, n_sub, o.bits.data_ptr(), o.intensity.data_ptr(), o.mse.data_ptr(), api._region(self.omega),
                        self.ws.data_ptr(), self.ws.numel(), self.comp.cuda_stream) for o in self.out]
+        if lut_seed is not None and before_each is not None:
+            raise ValueError("lut_seed (native a0) and before_each are exclusive")
+        if lut_seed is not None and lut is None:
+            raise ValueError("lut_seed needs the pool tensor `lut` to regenerate")
+        self._native = None
+        if before_each is None:          # the native sequencer (one C call per frame set)
+            slots = []
+            for d in range(depth):
+                o = self.out[d]
+                slots += [self.t_dev[d].data_ptr(), o.bits.data_ptr(), o.intensity.data_ptr(), o.mse.data_ptr(),
+                          self.bits_host[d].data_ptr(), self.mse_host[d].data_ptr(),
+                          self.inten_host[d].data_ptr() if self.inten_host is not None else 0]
+            self._slots = (C.c_void_p * len(slots))(*[C.c_void_p(p) if p else None for p in slots])
+            h = C.c_void_p()
+            with torch.cuda.device(dev):
+                check(lib().holo_ospr_stream_create(n, n_sub, depth, lp, L, 1 if lut_seed is not None else 0,
+                                                    (lut_seed or 0) & 0xFFFFFFFFFFFFFFFF, phase_offset,
+                                                    frame_stride, 1 if advance else 0, api._region(self.omega),
+                                                    self._slots, self.ws.data_ptr(), self.ws.numel(), C.byref(h)))
+            self._native = h
+            self._frame = C.c_int64()
+            hs = [C.c_void_p() for _ in range(3)]
+            check(lib().holo_ospr_stream_handles(h, *[C.byref(x) for x in hs]))
+            # the native streams, wrapped so that callers can record events on them (timing)
+            self.h2d, self.comp, self.d2h = [torch.cuda.ExternalStream(x.value, device=dev) for x in hs]
 
     def frame_offset(self, f: int) -> int:
         """Phase cursor of this stream's frame set f: off0 + f * frame_stride * N_SF N^2 when
@@ -86,6 +114,12 @@ class OsprStream:
     def submit(self, target_host: torch.Tensor) -> int:
         if target_host.dtype != torch.float32 or tuple(target_host.shape[-2:]) != (self.n, self.n):
             raise ValueError(f"target_host must be float32 [{self.n}][{self.n}]")
+        if self._native is not None:
+            if target_host.is_cuda or not target_host.is_contiguous():
+                raise ValueError("target_host must be a contiguous host tensor")
+            check(lib().holo_ospr_stream_submit(self._native, target_host.data_ptr(), C.byref(self._frame)))
+            self.f = self._frame.value + 1
+            return self._frame.value
         f = self.f
         s = f % self.depth
         if self.used[s]:
@@ -120,13 +154,37 @@ class OsprStream:
 
     def done(self, f: int) -> bool:
         """True once frame set f's outputs are in host memory (its target copy is complete too)."""
-        return self.d2h_done[self._slot(f)].query()
+        s = self._slot(f)
+        if self._native is not None:
+            r = lib().holo_ospr_stream_done(self._native, f)
+            if r < 0:
+                raise RuntimeError(lib().holo_last_error().decode())
+            return r == 1
+        return self.d2h_done[s].query()
 
     def result(self, f: int) -> Tuple[torch.Tensor, torch.Tensor, Optional[torch.Tensor]]:
         s = self._slot(f)
-        self.d2h_done[s].synchronize()
+        if self._native is not None:
+            check(lib().holo_ospr_stream_wait(self._native, f))
+        else:
+            self.d2h_done[s].synchronize()
         return self.bits_host[s], self.mse_host[s], (self.inten_host[s] if self.inten_host is not None else None)
 
     def drain(self) -> None:
         """Block until every submitted frame set is complete."""
-        self.d2h.synchronize()
+        if self._native is not None:
+            check(lib().holo_ospr_stream_drain(self._native))
+        else:
+            self.d2h.synchronize()
+
+    def close(self) -> None:
+        """Drain and release the native sequencer's streams and events (also done on deletion)."""
+        if getattr(self, "_native", None) is not None:
+            lib().holo_ospr_stream_destroy(self._native)
+            self._native = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

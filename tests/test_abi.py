@@ -189,3 +189,30 @@ def test_round2_entry_points_arg_errors(L):
     for q, tbl in ((0, FAKE), (17, FAKE), (8, None)):
         assert L.holo_ospr_generate_prng_table(FAKE, 64, 1, 8, 7, tbl, q, 0, 0, 8, None, FAKE, FAKE, om, FAKE, ws,
                                                None) == _lib.HOLO_ERR_INVALID_ARG
+
+
+def test_ospr_stream_arg_errors(L):
+    """The frame stream's create/submit checks run on the host before any CUDA call."""
+    h = C.c_void_p()
+    slots = (C.c_void_p * 7)(*([FAKE] * 6 + [None]))
+    ws_ok = L.holo_ospr_workspace_size(64, 1, 4)
+
+    def create(**kw):
+        a = dict(n=64, S=4, depth=1, lut=FAKE, nl=256, regen=0, slots=slots, ws=FAKE, wsb=ws_ok)
+        a.update(kw)
+        return L.holo_ospr_stream_create(a["n"], a["S"], a["depth"], a["lut"], a["nl"], a["regen"], 7, 0, 1, 1,
+                                         _region(1, 32, 0, 64), a["slots"], a["ws"], a["wsb"], C.byref(h))
+
+    assert create(n=100) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(S=0) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(depth=0) == _lib.HOLO_ERR_INVALID_ARG and create(depth=17) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(lut=None) == _lib.HOLO_ERR_INVALID_ARG                       # n_lut > 0 without a pool
+    assert create(lut=None, nl=0, regen=1) == _lib.HOLO_ERR_INVALID_ARG        # a0 needs a pool
+    assert create(slots=None) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(slots=(C.c_void_p * 7)(*([FAKE] * 3 + [None] + [FAKE] * 3))) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(ws=None) == _lib.HOLO_ERR_INVALID_ARG
+    assert create(wsb=ws_ok - 1) == _lib.HOLO_ERR_WORKSPACE
+    assert not h.value                                                          # nothing was created
+    assert L.holo_ospr_stream_submit(None, FAKE, None) == _lib.HOLO_ERR_INVALID_ARG
+    assert L.holo_ospr_stream_done(None, 0) == -1
+    L.holo_ospr_stream_destroy(None)                                            # no-op

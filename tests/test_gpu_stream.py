@@ -80,3 +80,31 @@ def test_stream_rejects_stale_frames():
     st.result(2)
     with pytest.raises(ValueError):
         st.submit(torch.zeros((32, 32), dtype=torch.float32))
+
+
+def test_native_a0_and_python_sequencer_agree():
+    """The native sequencer with a0 per frame set (lut_seed: holo_lut_generate into the pool on the
+    compute stream before each frame set) and the Python sequencer with the same a0 as a
+    before_each hook give the direct calls' holograms and MSE, bit for bit."""
+    n, S, L, off0 = 256, 6, 4099, 777
+    Ts = targets(n, 5, 900)
+    hosts = [torch.from_numpy(T).pin_memory() for T in Ts]
+    lut_a = torch.zeros(L, dtype=torch.complex64, device="cuda")          # garbage-free but not the pool
+    lut_b = torch.zeros(L, dtype=torch.complex64, device="cuda")
+    nat = hb.OsprStream(n, S, lut_a, depth=2, phase_offset=off0, lut_seed=LUT_SEED)
+    py = hb.OsprStream(n, S, lut_b, depth=2, phase_offset=off0,
+                       before_each=lambda: hb.lut_generate(LUT_SEED, L, out=lut_b))
+    assert nat._native is not None and py._native is None
+    ref_lut = hb.lut_generate(LUT_SEED, L)
+    for f, h in enumerate(hosts):
+        nat.submit(h)
+        py.submit(h)
+        b1, m1, _ = nat.result(f)
+        b2, m2, _ = py.result(f)
+        ref = hb.ospr_generate(torch.from_numpy(Ts[f]).cuda(), S, ref_lut, phase_offset=off0 + f * S * n * n)
+        assert torch.equal(b1, ref.bits[0].cpu()) and torch.equal(b2, ref.bits[0].cpu()), f
+        assert m1.item() == ref.mse.item() and m2.item() == ref.mse.item(), f
+    assert nat.done(len(hosts) - 1)
+    nat.close()
+    with pytest.raises(ValueError):
+        hb.OsprStream(n, S, lut_a, lut_seed=1, before_each=lambda: None)
