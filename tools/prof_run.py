@@ -30,6 +30,16 @@ if what == "c5":
         r = hb.ospr_generate(T, w.n_sub, lut)
     torch.cuda.synchronize()
     print("c5 mse", r.mse.item())
+if what == "n4096":                                   # R-26: one 4096^2 OSPR frame (N_SF = 4) and one GS iteration
+    from holo_synth import Region, blobs_target
+    n = 4096
+    T = torch.from_numpy(blobs_target(3, n, 16, n / 16, n / 6.4, Region.upper_half(n))[None]).to(dev)
+    lut = hb.lut_generate(LUT_SEED, 1 << 16)
+    for _ in range(reps):
+        r = hb.ospr_generate(T, 4, lut)
+        g = hb.gs_generate(T, 1, lut)
+    torch.cuda.synchronize()
+    print("n4096 mse", r.mse.item(), g.mse[0, 0].item())
 if what in ("all", "gs", "gs64"):
     w = WORKLOADS["C4"]
     nfr = w.frames if what == "gs64" else 8          # gs64: the whole C4 launch group (512 MiB state)
