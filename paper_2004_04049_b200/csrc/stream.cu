@@ -128,9 +128,23 @@ extern "C" holo_status holo_ospr_stream_create(int32_t n, int32_t n_sub, int32_t
             return cuda_status(e_, #call);                 \
     } while (0)
 
+static holo_status stream_submit(holo_ospr_stream *st, const float *target_host, int64_t *frame);
+
 extern "C" holo_status holo_ospr_stream_submit(holo_ospr_stream *st, const float *target_host, int64_t *frame)
 {
     HOLO_CHECK_ARG(st != nullptr && target_host != nullptr, "stream/target_host is NULL");
+    int cur = -1;   // the library's kernels launch on the current device: the stream's, for this call
+    HOLO_CUDA(cudaGetDevice(&cur));
+    if (cur != st->device)
+        HOLO_CUDA(cudaSetDevice(st->device));
+    const holo_status r = stream_submit(st, target_host, frame);
+    if (cur != st->device)
+        cudaSetDevice(cur);
+    return r;
+}
+
+static holo_status stream_submit(holo_ospr_stream *st, const float *target_host, int64_t *frame)
+{
     const int64_t f = st->f;
     const int s = (int)(f % st->depth);
     const size_t P = (size_t)st->n * st->n;
