@@ -34,6 +34,7 @@ from typing import Callable, Optional, Tuple
 import torch
 
 from . import api
+from ._lib import check
 
 
 def shard_range(n_units: int, world: int, rank: int) -> Tuple[int, int]:
@@ -210,8 +211,27 @@ class SubframeShardPipeline:
             self.gen_done = [torch.cuda.Event() for _ in range(depth)]
             self.slot_free = [torch.cuda.Event() for _ in range(depth)]
         self.f = 0
+        # the library calls with the default bindings go straight to the C ABI with arguments
+        # prepared once (the host must keep ahead of ~0.1 ms shards at 8 GPUs); the collectives
+        # stay torch.distributed (or the injected stand-ins)
+        self._fast = (self.cuda and generate is api.ospr_generate and finalize_rows is api.ospr_finalize_rows
+                      and mse_from_sums is api.ospr_mse_from_sums)
+        if self._fast:
+            lp, L = api._lut_args(lut)
+            self._lib, self._lutp, self._L = api.lib(), lp, L
+            self._reg = api._region(self.omega)
+            self._cs, self._ss = self.compute.cuda_stream, self.side.cuda_stream
 
     def _local(self, f: int, s: int):
+        if self._fast and self.sf[0] != self.sf[1]:
+            t = self.targets[s]
+            off = self.phase_offset + f * self.n_sub * self.n * self.n
+            b, e = (0, self.n_sub) if self.world == 1 else self.sf
+            check(self._lib.holo_ospr_generate(t.data_ptr(), self.n, 1, self.n_sub, self._lutp, self._L, off, b, e,
+                                               self.bits[s].data_ptr(), self.isum[s].data_ptr(),
+                                               self.mse[s].data_ptr() if self.world == 1 else None, self._reg,
+                                               self.ws.data_ptr(), self.ws.numel(), self._cs))
+            return
         out = api.OsprResult(bits=self.bits[s], intensity=self.isum[s],
                              mse=self.mse[s] if self.world == 1 else None)
         if self.sf[0] == self.sf[1]:     # no pair for this rank: a zero partial sum
@@ -225,11 +245,24 @@ class SubframeShardPipeline:
                           out=out)
 
     def _exchange(self, s: int):          # C-1, a7 on the owned rows, C-2, MSE
+        if self._fast:                    # (on the side stream: the caller's context)
+            r0, r1 = self.rows
+            mr, sm = self.mean_rows[s], self.sums[s]
+            self.sh.reduce_scatter(mr.view(-1), self.isum[s].view(-1))                                  # C-1
+            check(self._lib.holo_ospr_finalize_rows(self.targets[s].data_ptr(), mr.data_ptr(), self.n, r0, r1,
+                                                    self.n_sub, self._reg, mr.data_ptr(), sm.data_ptr(),
+                                                    self.ws_side.data_ptr(), self.ws_side.numel(), self._ss))  # a7
+            self.sh.all_reduce(sm)                                                                        # C-2
+            check(self._lib.holo_ospr_mse_from_sums(sm.data_ptr(), 1, self._reg, self.mse[s].data_ptr(), self._ss))
+            return
         self.sh.exchange(self.targets[s], self.isum[s], self.n_sub, self.mean_rows[s], self.sums[s], self.mse[s],
                          self.omega, fin_workspace=self.ws_side)
 
     def submit(self, target: torch.Tensor) -> int:
         """Queue frame self.f (target [N][N] on this rank's device); returns its index."""
+        if self._fast and (target.dtype != torch.float32 or not target.is_cuda or not target.is_contiguous()
+                           or target.numel() != self.n * self.n or target.device != self.dev):
+            raise ValueError(f"target must be a contiguous float32 [{self.n}][{self.n}] tensor on {self.dev}")
         f, s = self.f, self.f % self.depth
         self.targets[s] = target
         if not self.cuda:
