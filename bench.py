@@ -707,8 +707,7 @@ def c5_video(args, hb, world, rank, dev, flush):
     kw = {}
     if fake > 1:
         kw = dict(reduce_scatter=lambda o, i: o.copy_(i[:o.numel()]), all_reduce=lambda t: None)
-    pipe = SubframeShardPipeline(n5, S5, sworld, rank, lut5, depth=2,
-                                 before_each=lambda: hb.lut_generate(LUT_SEED, L5, out=lut5), **kw)
+    pipe = SubframeShardPipeline(n5, S5, sworld, rank, lut5, depth=2, lut_seed=LUT_SEED, **kw)   # a0 per frame
     kf = max(16, args.steps)                                   # frames streamed per timed run
     for f in range(max(args.warmup, 3)):
         pipe.submit(Ts[f % nt])

@@ -174,6 +174,7 @@ class SubframeShardPipeline:
 
     def __init__(self, n: int, n_sub: int, world: int, rank: int, lut: Optional[torch.Tensor],
                  device=None, depth: int = 2, omega=None, phase_offset: int = 0, before_each=None,
+                 lut_seed: Optional[int] = None,
                  generate: Callable = api.ospr_generate, finalize_rows: Callable = api.ospr_finalize_rows,
                  mse_from_sums: Callable = api.ospr_mse_from_sums,
                  reduce_scatter: Callable = _default_reduce_scatter,
@@ -221,6 +222,11 @@ class SubframeShardPipeline:
             self._lib, self._lutp, self._L = api.lib(), lp, L
             self._reg = api._region(self.omega)
             self._cs, self._ss = self.compute.cuda_stream, self.side.cuda_stream
+        if lut_seed is not None:         # a0 before each frame: the pool regenerated on the compute stream
+            if before_each is not None or lut is None or not self.cuda:
+                raise ValueError("lut_seed needs a CUDA pool `lut` and no before_each")
+            fn, ptr, n_lut, cs = api.lib().holo_lut_generate, lut.data_ptr(), lut.numel(), self.compute.cuda_stream
+            self.before_each = lambda: check(fn(lut_seed & 0xFFFFFFFFFFFFFFFF, n_lut, ptr, cs))
 
     def _local(self, f: int, s: int):
         if self._fast and self.sf[0] != self.sf[1]:
