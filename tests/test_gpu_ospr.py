@@ -221,6 +221,14 @@ def test_ospr_single_subframe_and_flat():
     assert all(np.array_equal(b[0], b[s]) for s in range(4))
 
 
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_ospr_single_subframe_fused_a7(n):
+    """N_SF = 1 at the sizes with a7 fused into pass C: one unpaired sub-frame (h'_b = 0), the
+    mirrored row-pair epilogue and its ticket on a single pair (P-3/P-4/P-5)."""
+    T = blobs_target(21 + n, n, 16, n / 16, n / 6.4, Region.upper_half(n))
+    ospr_parity(T, 1, 10007, offset=31)
+
+
 def test_ospr_shards_reproduce_single_call():
     """P-8 on one GPU: shard ranges with global draw indices give bit-identical
     holograms, and finalize(sum of partial sums) matches the single call."""
