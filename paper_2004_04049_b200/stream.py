@@ -84,6 +84,7 @@ class OsprStream:
         if lut_seed is not None and lut is None:
             raise ValueError("lut_seed needs the pool tensor `lut` to regenerate")
         self._native = None
+        self._closed = False
         if before_each is None:          # the native sequencer (one C call per frame set)
             slots = []
             for d in range(depth):
@@ -114,6 +115,8 @@ class OsprStream:
     def submit(self, target_host: torch.Tensor) -> int:
         if target_host.dtype != torch.float32 or tuple(target_host.shape[-2:]) != (self.n, self.n):
             raise ValueError(f"target_host must be float32 [{self.n}][{self.n}]")
+        if self._closed:
+            raise RuntimeError("the stream is closed")
         if self._native is not None:
             if target_host.is_cuda or not target_host.is_contiguous():
                 raise ValueError("target_host must be a contiguous host tensor")
@@ -148,6 +151,8 @@ class OsprStream:
         return f
 
     def _slot(self, f: int) -> int:
+        if self._closed:
+            raise RuntimeError("the stream is closed")
         if not (self.f - self.depth <= f < self.f):
             raise ValueError(f"frame set {f} is not among the last {self.depth} submitted")
         return f % self.depth
@@ -172,6 +177,8 @@ class OsprStream:
 
     def drain(self) -> None:
         """Block until every submitted frame set is complete."""
+        if self._closed:
+            return
         if self._native is not None:
             check(lib().holo_ospr_stream_drain(self._native))
         else:
@@ -182,6 +189,7 @@ class OsprStream:
         if getattr(self, "_native", None) is not None:
             lib().holo_ospr_stream_destroy(self._native)
             self._native = None
+            self._closed = True
 
     def __del__(self):
         try:

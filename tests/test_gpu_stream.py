@@ -106,5 +106,7 @@ def test_native_a0_and_python_sequencer_agree():
         assert m1.item() == ref.mse.item() and m2.item() == ref.mse.item(), f
     assert nat.done(len(hosts) - 1)
     nat.close()
+    with pytest.raises(RuntimeError):
+        nat.submit(hosts[0])                     # the native streams are gone
     with pytest.raises(ValueError):
         hb.OsprStream(n, S, lut_a, lut_seed=1, before_each=lambda: None)
