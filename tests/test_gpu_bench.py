@@ -37,3 +37,25 @@ def test_bench_json_contract():
     assert e["d2h_bytes_per_step"] == 24 * 1024 * 128 + 8        # packed holograms + the MSE
     assert d["gpu_launches"] >= 3 * 4                             # a0 + three passes per step
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+@pytest.mark.parametrize("env,args,key", [
+    ({"HOLO_BENCH_FAKE_WORLD": "4"}, ["--no-c5", "--no-e2e"], None),          # C3 split over 4 "ranks"
+    ({"HOLO_BENCH_FAKE_SHARDS": "4"}, ["--no-e2e"], "c5_video"),              # C5 video, 4-way shards
+])
+def test_bench_sharded_step_structures(env, args, key):
+    """The N > 1 step structures (sub-frame shards, the exchange around the graphed shard, the
+    video pipeline's side stream) run on one GPU with stand-in collectives (testing hooks of
+    bench.py); the line stays well formed."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3", "--no-sweep",
+                        "--no-gs"] + args, capture_output=True, text=True, cwd=ROOT, timeout=900,
+                       env=dict(os.environ, **env))
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")][-1])
+    assert d["value"] > 0
+    if key:
+        v = d[key]
+        assert v["value"] > 0 and "FAKE" in v["config"]["partition"]
+        assert v["shard"]["sub_frames"][1] - v["shard"]["sub_frames"][0] == 8     # 32 sub-frames / 4
+    else:
+        assert "sub-frame shards x4" in d["config"]["parallelism"]

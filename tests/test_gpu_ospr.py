@@ -126,7 +126,7 @@ def test_pass_a_pairs_prng_table_match_oracle(n, q, offset):
         assert np.max(np.abs(Z[j] - ref)) <= 2.0 ** -20, (n, q, s)
 
 
-@pytest.mark.parametrize("n,S,q", [(64, 5, 8), (256, 4, 12), (1024, 6, 16)])
+@pytest.mark.parametrize("n,S,q", [(64, 5, 8), (256, 4, 12), (1024, 6, 16), (2048, 3, 8)])
 def test_ospr_prng_table_against_oracle(n, S, q):
     """The whole OSPR path with the table source: bits against the oracle's fp64 IDFT of its
     quantised-source randomisation (P-3 band), intensity conditional on the GPU bits (P-4),
